@@ -1,0 +1,497 @@
+#!/usr/bin/env python
+"""Throughput bench of the B200 2D-frontend hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                    [--frames-per-step F] [--impl reference]
+
+A *step* = one pass of the whole path (pyramid -> GFTT/NMS/top-k -> KLT) over
+F consecutive frames of every camera of the workload (B = F*C camera-frames),
+read from a device-resident ring of rendered frames larger than L2.  `value`
+is camera-frames/s over all ranks (max-over-ranks device time); `e2e` is the
+same metric with each step's frames copied from pinned host memory and its
+results (keypoints, tracked positions, statuses) read back inside the timed
+region.  N > 1: one process per GPU (torchrun), each rank processes its own
+frame chunk of the stream (weak scaling) and the per-step track lists are
+all-gathered over NCCL on a side stream.
+
+--impl reference times the oracle (oracle/, plain single-threaded C) on the
+host on the same workload: each step = one camera-frame.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import shutil
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+DEFAULT_CONFIG = "c2"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--frames-per-step", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = {"hbm_gbs": 6537.3, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        p.update({k: m[k] for k in ("hbm_gbs", "sm_max_mhz") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    # FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 flop/FMA x max SM clock
+    p["fp32_tflops"] = 148 * 128 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    return p
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work models
+# ---------------------------------------------------------------------------
+def level_pixels(W, H, levels):
+    return [(W >> L) * (H >> L) for L in range(levels)]
+
+
+def alg_bytes_pyramid(W, H, levels):
+    """K1 compulsory traffic per image: read u8 L0, write fp32 levels >= 1."""
+    lp = level_pixels(W, H, levels)
+    return W * H + 4 * sum(lp[1:])
+
+
+def alg_bytes_full_path(W, H, levels):
+    """Whole path per camera-frame: read new u8 frame, write its
+    fp32 levels, read previous u8 frame + fp32 levels for KLT."""
+    lp = level_pixels(W, H, levels)
+    return 2 * W * H + 2 * 4 * sum(lp[1:])
+
+
+KLT_FLOP_LEVEL = 55   # per window pixel per level with a template
+KLT_FLOP_STEP = 11    # per window pixel per Gauss-Newton step
+
+
+def klt_flops(iters_packed: np.ndarray, win: int) -> float:
+    n = win * win
+    steps = (iters_packed & 0xFFFFFF).astype(np.int64)
+    lv = (iters_packed >> 24).astype(np.int64)
+    return float(n * (KLT_FLOP_LEVEL * lv.sum() + KLT_FLOP_STEP * steps.sum()))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.idx = gpu_index
+        if shutil.which("nvidia-smi"):
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+class OracleStream:
+    """The oracle run as a frame stream: per camera-frame, pyramid(cur) +
+    detect(cur) + KLT(prev -> cur) of the previous frame's keypoints, the
+    same work one camera-frame costs on the GPU path."""
+
+    def __init__(self, wl, n_frames=8, salt=0):
+        import oracle
+        self.o, self.wl = oracle, wl
+        st = synth.make_stream(wl, n_frames, "cpu", cams=[0], rank_salt=salt)
+        self.frames = [st.frames[0, t, :, :wl.W].numpy().copy() for t in range(n_frames)]
+        self.t = 0
+        _, self.prev_pyr = oracle.build_pyramid(self.frames[0], wl.levels)
+        self.prev_pts = self._detect(self.frames[0])
+
+    def _detect(self, img):
+        wl = self.wl
+        xy, _, _ = self.o.detect_gftt(img, wl.grid_x, wl.grid_y, k=wl.k, K_min=wl.K_min,
+                                      border=wl.border)
+        return xy.reshape(-1, 2)
+
+    def step(self):
+        wl, o = self.wl, self.o
+        self.t = (self.t + 1) % len(self.frames)
+        cur = self.frames[self.t]
+        _, cur_pyr = o.build_pyramid(cur, wl.levels)
+        pts = self._detect(cur)
+        pos, st, nc, dg = o.track_klt(self.prev_pyr, cur_pyr, wl.W, wl.H, wl.levels,
+                                      self.prev_pts, win=wl.win, iters=wl.iters, eps=wl.eps,
+                                      ncc_min=wl.ncc_min, min_eig=wl.min_eig)
+        tracked, attempted = int((st == 0).sum()), int((st != 4).sum())
+        self.prev_pyr, self.prev_pts = cur_pyr, pts
+        return tracked, attempted
+
+
+def time_oracle(wl, seconds: float, max_frames: int = 64):
+    """Camera-frames per second of the oracle on one host core."""
+    os_ = OracleStream(wl)
+    n, tracked, t0 = 0, 0, time.perf_counter()
+    while True:
+        tr, _ = os_.step()
+        tracked += tr
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or n >= max_frames:
+            break
+    return {"frames": n, "seconds": el, "tracked": tracked}
+
+
+def cpu_cores_used():
+    return 1  # the oracle is single-threaded (plain C, no threads)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = synth.WORKLOADS[args.config]
+    import oracle
+    oracle.build()
+    ostream = OracleStream(wl)
+    times, tracked = [], 0
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        tr, _ = ostream.step()
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            tracked += tr
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": "frames/s (camera-frames, detect+KLT)", "value": value,
+        "unit": "camera-frames/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(wl, 1, 1, args.gpus),
+        "keypoints_tracked_per_s": tracked / total,
+        "cpu_baseline": {"value": value, "unit": "camera-frames/s", "cores": cpu_cores_used(),
+                         "kind": "oracle",
+                         "sample": f"{args.steps} consecutive camera-frames of {wl.name} "
+                                   f"(camera 0, 8-frame cycle), one step = one camera-frame"},
+        "e2e": {"value": value, "unit": "camera-frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def workload_config(wl, F, C, n_gpus, ring=None):
+    k = wl.k or (wl.K_min // (wl.grid_x * wl.grid_y) + 1)
+    cfg = {"workload": f"{wl.name}: {wl.description}", "cams": wl.cams, "W": wl.W, "H": wl.H,
+           "levels": wl.levels, "grid": [wl.grid_x, wl.grid_y], "K_min": wl.K_min, "k": k,
+           "slots_per_image": wl.grid_x * wl.grid_y * k, "win": wl.win, "iters": wl.iters,
+           "frames_per_step": F, "images_per_step": F * C,
+           "parallelism": f"dp{n_gpus} (frame-chunk shards, one process per GPU)"}
+    if ring is not None:
+        cfg.update(ring)
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import Frontend2D, RingSchedule
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = synth.WORKLOADS[args.config]
+    C = wl.cams
+    F = args.frames_per_step or max(1, 32 // C)
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    fe = Frontend2D(cfg, C, F, dev, wl.pitch)
+    B, P = fe.B, fe.P
+
+    # ring of rendered frames in HBM, larger than L2 (2.5x), multiple of 2F
+    rig_bytes = C * wl.H * wl.pitch
+    R = max(2 * F, math.ceil(2.5 * L2_BYTES / rig_bytes))
+    R = (R + 2 * F - 1) // (2 * F) * (2 * F)
+    t_render = time.perf_counter()
+    stream = synth.make_stream(wl, R, dev, rank_salt=rank)
+    torch.cuda.synchronize()
+    t_render = time.perf_counter() - t_render
+    sched = RingSchedule(stream.frames, F)
+    ring_info = {"ring_frames": R, "ring_bytes": int(stream.frames.numel()),
+                 "l2": f"inputs larger than L2: ring {stream.frames.numel() / 2**20:.0f} MiB "
+                       f"> 126 MiB L2, each step reads new frames"}
+
+    # multi-GPU: per-step track lists gathered on a side stream (double-buffered)
+    side = torch.cuda.Stream(device=dev) if world > 1 else None
+    pos_buf = [torch.zeros((B, P, 2), device=dev) for _ in range(2)]
+    st_buf = [torch.zeros((B, P), dtype=torch.uint8, device=dev) for _ in range(2)]
+    gathered_pos = [torch.empty((world * B, P, 2), device=dev) for _ in range(2)] if world > 1 else None
+    gathered_st = [torch.empty((world * B, P), dtype=torch.uint8, device=dev) for _ in range(2)] if world > 1 else None
+    gather_done = [None, None]
+
+    n_total = args.warmup + args.steps
+    status_log = torch.zeros((args.steps, B, P), dtype=torch.uint8, device=dev)
+    iters_log = torch.zeros((args.steps, B, P), dtype=torch.int32, device=dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def one_step(s, timed_index=None):
+        cur, prev, parity = sched.tables(s)
+        slot = s % 2
+        if world > 1 and gather_done[slot] is not None:
+            torch.cuda.current_stream().wait_event(gather_done[slot])
+        evs = ev[timed_index] if timed_index is not None else None
+        fe.pos = pos_buf[slot]
+        fe.step(cur, prev, parity, status_out=st_buf[slot], events=evs)
+        if timed_index is not None:
+            status_log[timed_index].copy_(st_buf[slot], non_blocking=True)
+            iters_log[timed_index].copy_(fe.iters, non_blocking=True)
+        if world > 1:
+            done = torch.cuda.Event()
+            done.record()
+            with torch.cuda.stream(side):
+                side.wait_event(done)
+                dist.all_gather_into_tensor(gathered_pos[slot], pos_buf[slot])
+                dist.all_gather_into_tensor(gathered_st[slot], st_buf[slot])
+                e = torch.cuda.Event()
+                e.record(side)
+                gather_done[slot] = e
+
+    fe.prime(sched.before_first, 1)
+    for s in range(args.warmup):
+        one_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in range(args.steps):
+        one_step(args.warmup + i, timed_index=i)
+    if world > 1:
+        for e in gather_done:
+            if e is not None:
+                torch.cuda.current_stream().wait_event(e)
+    end.record()
+    torch.cuda.synchronize()
+    clock_rec = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # per-kernel device times (CUDA events on the launching stream)
+    names = ["pyramid", "gftt_topk", "klt"]
+    kt = np.array([[ev[i][j].elapsed_time(ev[i][j + 1]) for j in range(3)]
+                   for i in range(args.steps)])
+    k_ms = kt.mean(axis=0)
+
+    tracked = int((status_log == 0).sum().item())
+    attempted = int((status_log != 4).sum().item())
+    iters_np = iters_log.cpu().numpy()
+    frames_total = world * B * args.steps
+    value = frames_total / (ms_max / 1e3)
+    tr_t = torch.tensor([tracked, attempted], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tr_t)
+    tracked_all, attempted_all = float(tr_t[0].item()), float(tr_t[1].item())
+
+    pk = peaks()
+    # roofline of the dominant kernel
+    dom = int(np.argmax(k_ms))
+    if names[dom] == "pyramid":
+        alg = B * alg_bytes_pyramid(wl.W, wl.H, wl.levels)
+        ach = alg / (k_ms[dom] * 1e-3) / 1e9
+        roof = {"kernel": "pyramid", "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / pk["hbm_gbs"], "traffic": None}
+    elif names[dom] == "klt":
+        fl = klt_flops(iters_np, wl.win) / args.steps
+        ach = fl / (k_ms[dom] * 1e-3) / 1e12
+        roof = {"kernel": "klt", "bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"],
+                "unit": "TFLOP/s", "frac": ach / pk["fp32_tflops"], "traffic": None,
+                "model": f"{KLT_FLOP_LEVEL}*n per level + {KLT_FLOP_STEP}*n per GN step, "
+                         f"n=win^2, counts from the kernel's iters_out"}
+    else:
+        ops = B * wl.W * wl.H * 40.0
+        ach = ops / (k_ms[dom] * 1e-3) / 1e12
+        peak_ops = pk["fp32_tflops"] / 2
+        roof = {"kernel": "gftt_topk", "bound": "alu", "achieved": ach, "peak": peak_ops,
+                "unit": "Tlane-op/s", "frac": ach / peak_ops, "traffic": None,
+                "model": "40 lane-ops per L0 pixel"}
+    traffic_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(traffic_path):
+        tr = json.load(open(traffic_path))
+        if roof["kernel"] in tr:
+            roof["traffic"] = tr[roof["kernel"]]
+    full_bytes = alg_bytes_full_path(wl.W, wl.H, wl.levels) * frames_total
+    hbm_ach = full_bytes / (ms_max / 1e3) / 1e9 / world
+
+    line = {
+        "metric": "frames/s (camera-frames, detect+KLT)", "value": value,
+        "unit": "camera-frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(wl, F, C, world, ring_info),
+        "keypoints_tracked_per_s": tracked_all / (ms_max / 1e3),
+        "keypoints_attempted_per_s": attempted_all / (ms_max / 1e3),
+        "rig_frames_per_s": value / C,
+        "hbm_full_path": {"achieved_GBps_per_gpu": hbm_ach, "frac_of_measured": hbm_ach / pk["hbm_gbs"],
+                          "frac_of_8TBps_spec": hbm_ach / 8000.0,
+                          "alg_bytes_per_camera_frame": alg_bytes_full_path(wl.W, wl.H, wl.levels)},
+        "roofline": roof,
+        "kernels": {n: {"ms_per_launch": float(k_ms[j]), "share_of_step": float(k_ms[j] / (ms / args.steps))}
+                    for j, n in enumerate(names)},
+        "gpu_launches": 3 * args.steps,
+        "peaks": pk,
+        "clocks": clock_rec,
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = run_e2e(fe, stream.frames, sched, args, dev, F, C)
+    elif rank == 0:
+        line["e2e"] = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ob = time_oracle(wl, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": ob["frames"] / ob["seconds"], "unit": "camera-frames/s",
+            "cores": cpu_cores_used(), "kind": "oracle",
+            "sample": f"{ob['frames']} consecutive camera-frames of {wl.name} (camera 0): "
+                      f"pyramid + detect + KLT of {P} slots each, {ob['seconds']:.1f} s on "
+                      f"one host core",
+            "host_nproc": os.cpu_count()}
+    if rank == 0:
+        line["render_seconds"] = t_render
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(fe, ring, sched, args, dev, F, C):
+    """Same metric through the public API with host buffers: per step, H2D of the
+    step's frames from pinned memory + the three launches + D2H of keypoints,
+    tracked positions and statuses."""
+    import torch
+
+    from paper_2506_04359_b200 import vslam2d as v2d
+    B, H, pitch = F * C, ring.shape[2], ring.shape[3]
+    n_host = 4
+    # pinned host frames: n_host steps worth, batch order f*C + c
+    host = torch.empty((n_host, B, H, pitch), dtype=torch.uint8, pin_memory=True)
+    for s in range(n_host):
+        for f in range(F):
+            for c in range(C):
+                host[s, f * C + c].copy_(ring[c, (s * F + f) % ring.shape[1]])
+    dbuf = torch.empty((2, B, H, pitch), dtype=torch.uint8, device=dev)
+    cur_t = [v2d.ptrs_of(dbuf[i]) for i in range(2)]
+    prev_t = []
+    for i in range(2):
+        pv = torch.empty_like(cur_t[i])
+        pv[C:] = cur_t[i][:-C]
+        pv[:C] = cur_t[1 - i][-C:]
+        prev_t.append(pv)
+    kp_h = torch.empty((F, C, fe.P, 2), dtype=torch.float32, pin_memory=True)
+    pos_h = torch.empty((B, fe.P, 2), dtype=torch.float32, pin_memory=True)
+    st_h = torch.empty((B, fe.P), dtype=torch.uint8, pin_memory=True)
+    h2d = B * H * pitch
+    d2h = kp_h.numel() * 4 + pos_h.numel() * 4 + st_h.numel()
+
+    def step(s):
+        i = s % 2
+        dbuf[i].copy_(host[s % n_host], non_blocking=True)
+        fe.step(cur_t[i], prev_t[i], i)
+        kp_h.copy_(fe.kp_xy[1:], non_blocking=True)
+        pos_h.copy_(fe.pos, non_blocking=True)
+        st_h.copy_(fe.status, non_blocking=True)
+
+    dbuf[1].copy_(host[n_host - 1], non_blocking=True)
+    fe.prime(cur_t[1][-C:], 1)
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for s in range(args.steps):
+        step(args.warmup + s)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    return {"value": B * args.steps / (ms / 1e3), "unit": "camera-frames/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms / args.steps}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

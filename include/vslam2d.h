@@ -1,0 +1,139 @@
+/*
+ * vslam2d.h — C ABI of the B200-native cuVSLAM 2D-module hot path.
+ *
+ * Path (§2.1 "2D module"):
+ *   per camera-frame: image pyramid -> Sobel -> Shi-Tomasi (GFTT) response ->
+ *   3x3 NMS + per-cell top-k over an N x M grid (Eq. 1) ; then pyramidal
+ *   Lucas-Kanade (KLT) of the previous frame's keypoints into this frame with
+ *   a per-level NCC gate.
+ *
+ * Conventions for every entry point
+ *   - All image / keypoint buffers are CALLER-OWNED DEVICE memory (cudaMalloc /
+ *     torch).  Arrays named `*_ptrs` are DEVICE arrays of B device pointers, one
+ *     per image, so ring slots and camera buffers are addressed without copies.
+ *   - The library never allocates, frees or synchronises and keeps no global
+ *     state: calls are thread-safe and ordered on `stream` (a cudaStream_t;
+ *     NULL = legacy default stream).  Work is enqueued asynchronously.
+ *   - Return value 0 = enqueued.  Negative codes: V2D_EINVAL (bad argument;
+ *     nothing enqueued), V2D_EALIGN (pitch/alignment contract violated;
+ *     nothing enqueued), V2D_ECUDA (launch failed, from cudaGetLastError;
+ *     asynchronous faults surface at the caller's next synchronisation).
+ *     Per-keypoint outcomes are never errors: they are statuses.
+ *   - Coordinates: x = column in [0,W), y = row in [0,H); pixel centres are
+ *     integers; intensities are raw u8 values 0..255 (reading #3).
+ *
+ * Every call is implemented by hand-written sm_100a kernels in
+ * paper_2506_04359_b200/csrc; there is no CPU fallback.
+ */
+#ifndef VSLAM2D_H
+#define VSLAM2D_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* v2d_stream_t; /* identical to cudaStream_t */
+
+#define V2D_OK 0
+#define V2D_EINVAL (-1)
+#define V2D_EALIGN (-2)
+#define V2D_ECUDA (-3)
+
+#define V2D_MAX_LEVELS 8
+#define V2D_MAX_K 256
+#define V2D_MAX_WIN 29
+
+/* KLT status codes.  LOST_* and SKIPPED slots get pos (-1,-1). */
+#define V2D_TRACKED 0
+#define V2D_LOST_OOB 1       /* left the image (any L0 iterate, or final pos outside the r-margin) */
+#define V2D_LOST_NCC 2       /* NCC_L < ncc_min at some level ("NCC check") */
+#define V2D_LOST_SMALL_EIG 3 /* lambda_min(G)/n < min_eig at level 0 */
+#define V2D_SKIPPED 4        /* input slot empty (-1,-1) / non-finite, or in_status != 0 */
+
+/* Pyramid layout of ONE image's levels 1..levels-1 (level 0 is the caller's u8
+ * frame).  Level L (L >= 1) is a dense fp32 plane of W[L] x H[L] with row pitch
+ * pitch[L] = round_up(W[L], 32) floats (128-B rows), at float offset offset[L]
+ * from the image's pyramid base pointer.  floats_per_image = total size;
+ * every offset is a multiple of 32 floats.  pitch[0]/offset[0] are 0. */
+typedef struct {
+  int levels;
+  int W[V2D_MAX_LEVELS];
+  int H[V2D_MAX_LEVELS];
+  int64_t pitch[V2D_MAX_LEVELS];
+  int64_t offset[V2D_MAX_LEVELS];
+  int64_t floats_per_image;
+} v2d_layout;
+
+/* Host-only.  Level sizes W_L = floor(W_{L-1}/2).
+ * V2D_EINVAL unless 1 <= levels <= 8, W>>(levels-1) >= 1 and H>>(levels-1) >= 1
+ * ("too many levels for image size"), or out == NULL. */
+int v2d_pyramid_layout(int W, int H, int levels, v2d_layout* out);
+
+/* Host-only.  Eq. 1: "k > floor(K_I/(N*M))".  k == 0 resolves to
+ * floor(K_min/(grid_x*grid_y)) + 1; k > 0 is validated against the
+ * same inequality and against V2D_MAX_K.  *k_out receives the per-cell k. */
+int v2d_grid_k(int grid_x, int grid_y, int k, int K_min, int* k_out);
+
+/* Image pyramid ("each image pyramid level"; reading #1: 2x2 box, floor
+ * halving).  For each of B images: level L = mean of the 2x2 block of
+ * level L-1, computed in one pass as the exact mean of the aligned 2^L x 2^L
+ * L0 block (bit-exact: values lie in 4^-L * Z).
+ *   l0_ptrs   device array [B] of u8 frames, row pitch l0_pitch bytes
+ *   pyr_ptrs  device array [B] of fp32 pyramid bases (v2d_layout of W,H,levels)
+ * V2D_EALIGN: l0_pitch % 16 != 0 or l0_pitch < W.  levels == 1 enqueues nothing. */
+int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
+                      int levels, float* const* pyr_ptrs, v2d_stream_t stream);
+
+/* Keypoint selection: Sobel/8 gradients, 3x3 structure-tensor
+ * response R = lambda_min (fp32 contract, reading #4), eligibility
+ * border <= x <= W-1-border (same for y) and R > min_score, optional strict
+ * 3x3 NMS on the key (bits(R) << 32 | ~(y*W+x)) (reading #5), and per cell of
+ * the grid_x x grid_y floor partition the top-k candidates by that key
+ * (reading #6/#8).  k resolves via v2d_grid_k.
+ *   kp_xy      [B][grid_y][grid_x][k][2] fp32 (x,y); unfilled slots (-1,-1)
+ *   kp_score   [B][grid_y][grid_x][k]    fp32 R; unfilled 0
+ *   cell_count [B][grid_y*grid_x]        int32 filled slots per cell
+ *   resp       nullable [B][H][W] fp32: full R map (0 outside 2..W-3 x 2..H-3);
+ *              when given, the lazy-eigenvalue shortcut is disabled.
+ * V2D_EINVAL: border < 3, W or H < 2*border+1, grid cell < 1 px, bad k, nms not
+ * 0/1, W*H >= 2^31.  V2D_EALIGN: l0_pitch % 16 != 0. */
+int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
+                    int grid_x, int grid_y, int k, int K_min, float min_score, int border,
+                    int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
+                    v2d_stream_t stream);
+
+/* Pyramidal LK tracking (LK_1981, LK_2000; reading of SURVEY §8(c) D7):
+ * forward-additive Gauss-Newton with template gradients, coarse-to-fine over
+ * `levels`, at most `iters` steps per level (stop when |eta| < eps, level px),
+ * NCC(template, warped patch) >= ncc_min required after every level, window
+ * win x win (odd, 3..V2D_MAX_WIN).  Image b's keypoints pts[b] (L0 px, in the
+ * PREVIOUS frame) are tracked from (prev_l0_ptrs[b], prev_pyr_ptrs[b]) into
+ * (next_l0_ptrs[b], next_pyr_ptrs[b]); pyramids as built by v2d_build_pyramid.
+ *   pts        [B][P][2] fp32; (-1,-1) = empty slot -> V2D_SKIPPED
+ *   guess      nullable [B][P][2] fp32 displacement prior (L0 px)
+ *   in_status  nullable [B][P] u8; non-zero -> V2D_SKIPPED (lost is terminal)
+ *   out_pos    [B][P][2] fp32 tracked position, (-1,-1) unless V2D_TRACKED
+ *   status     [B][P] u8 V2D_* status
+ *   ncc        nullable [B][P] fp32 last evaluated NCC (0 if none)
+ *   iters_out  nullable [B][P] int32 work counters: bits 0..23 = Gauss-Newton
+ *              steps over all levels, bits 24..31 = levels whose template was built
+ * min_eig is in (gray/px)^2 per window pixel: lost at L0 when lambda_min(G)/n
+ * < min_eig; coarse levels are skipped instead (reading #15). */
+int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_pyr_ptrs,
+                  const uint8_t* const* next_l0_ptrs, const float* const* next_pyr_ptrs,
+                  int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
+                  const float* guess, const uint8_t* in_status, int P, int win, int iters,
+                  float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
+                  float* ncc, int32_t* iters_out, v2d_stream_t stream);
+
+/* Static string for a V2D_* return code. */
+const char* v2d_strerror(int code);
+
+/* ABI version (major*100 + minor). */
+int v2d_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSLAM2D_H */

@@ -1,0 +1,129 @@
+// abi.cu — the extern "C" boundary declared in include/vslam2d.h: argument
+// validation, layout arithmetic and kernel launches.  No computation of the
+// method happens here (it is all in pyramid.cu, gftt.cu, klt.cu).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+// D1 level sizes + fp32 layout of levels 1..L-1 (128-B rows, 128-B aligned levels).
+int make_levels(int W, int H, int levels, v2d::Levels* lv, int64_t* total) {
+  if (W < 1 || H < 1 || levels < 1 || levels > V2D_MAX_LEVELS) return V2D_EINVAL;
+  if ((W >> (levels - 1)) < 1 || (H >> (levels - 1)) < 1) return V2D_EINVAL;
+  int64_t off = 0;
+  lv->n = levels;
+  for (int L = 0; L < V2D_MAX_LEVELS; ++L) {
+    lv->W[L] = L < levels ? (W >> L) : 0;
+    lv->H[L] = L < levels ? (H >> L) : 0;
+    lv->pitch[L] = 0;
+    lv->offset[L] = 0;
+    if (L >= 1 && L < levels) {
+      lv->pitch[L] = v2d::round_up64(lv->W[L], 32);
+      lv->offset[L] = off;
+      off += lv->pitch[L] * lv->H[L];
+    }
+  }
+  if (total) *total = off;
+  return V2D_OK;
+}
+
+int grid_k(int gx, int gy, int k, int K_min, int* k_out) {
+  if (gx < 1 || gy < 1 || k < 0 || K_min < 0) return V2D_EINVAL;
+  const int64_t q = (int64_t)K_min / ((int64_t)gx * gy);  // floor(K_I/(N*M)), Eq. 1
+  const int64_t kk = k == 0 ? q + 1 : k;
+  if (kk <= q || kk > V2D_MAX_K) return V2D_EINVAL;
+  if (k_out) *k_out = (int)kk;
+  return V2D_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int v2d_version(void) { return 100; }
+
+const char* v2d_strerror(int code) {
+  switch (code) {
+    case V2D_OK: return "ok";
+    case V2D_EINVAL: return "invalid argument";
+    case V2D_EALIGN: return "pitch or alignment contract violated";
+    case V2D_ECUDA: return "CUDA launch error";
+    default: return "unknown error";
+  }
+}
+
+int v2d_pyramid_layout(int W, int H, int levels, v2d_layout* out) {
+  if (!out) return V2D_EINVAL;
+  v2d::Levels lv;
+  int64_t total = 0;
+  const int rc = make_levels(W, H, levels, &lv, &total);
+  if (rc) return rc;
+  out->levels = levels;
+  for (int L = 0; L < V2D_MAX_LEVELS; ++L) {
+    out->W[L] = lv.W[L];
+    out->H[L] = lv.H[L];
+    out->pitch[L] = lv.pitch[L];
+    out->offset[L] = lv.offset[L];
+  }
+  out->floats_per_image = total;
+  return V2D_OK;
+}
+
+int v2d_grid_k(int grid_x, int grid_y, int k, int K_min, int* k_out) {
+  return grid_k(grid_x, grid_y, k, K_min, k_out);
+}
+
+int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
+                      int levels, float* const* pyr_ptrs, v2d_stream_t stream) {
+  v2d::Levels lv;
+  if (B < 0 || B > 65535 || (B > 0 && (!l0_ptrs || !pyr_ptrs))) return V2D_EINVAL;
+  if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
+  if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
+  return v2d::launch_pyramid(l0_ptrs, l0_pitch, B, W, H, lv, pyr_ptrs,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
+                    int grid_x, int grid_y, int k, int K_min, float min_score, int border,
+                    int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
+                    v2d_stream_t stream) {
+  int kk = 0;
+  if (B < 0 || B > 65535) return V2D_EINVAL;
+  if (B > 0 && (!l0_ptrs || !kp_xy || !kp_score || !cell_count)) return V2D_EINVAL;
+  if (W < 1 || H < 1 || (int64_t)W * H >= ((int64_t)1 << 31)) return V2D_EINVAL;
+  if (border < 3 || W < 2 * border + 1 || H < 2 * border + 1) return V2D_EINVAL;
+  if (grid_x < 1 || grid_y < 1 || grid_x > W || grid_y > H) return V2D_EINVAL;
+  if ((int64_t)grid_x * grid_y > 65535 * 16) return V2D_EINVAL;
+  if (nms != 0 && nms != 1) return V2D_EINVAL;
+  if (std::isnan(min_score)) return V2D_EINVAL;
+  if (grid_k(grid_x, grid_y, k, K_min, &kk)) return V2D_EINVAL;
+  if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
+  v2d::GfttArgs a{W, H, grid_x, grid_y, kk, border, nms, min_score, l0_pitch};
+  return v2d::launch_gftt(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_pyr_ptrs,
+                  const uint8_t* const* next_l0_ptrs, const float* const* next_pyr_ptrs,
+                  int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
+                  const float* guess, const uint8_t* in_status, int P, int win, int iters,
+                  float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
+                  float* ncc, int32_t* iters_out, v2d_stream_t stream) {
+  v2d::Levels lv;
+  if (B < 0 || P < 0) return V2D_EINVAL;
+  if ((int64_t)B * P > ((int64_t)1 << 40)) return V2D_EINVAL;
+  if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
+  if (win < 3 || win > V2D_MAX_WIN || (win % 2) == 0 || iters < 1) return V2D_EINVAL;
+  if (!(eps >= 0.0f) || std::isnan(ncc_min) || std::isnan(min_eig)) return V2D_EINVAL;
+  if ((int64_t)B * P > 0 && (!prev_l0_ptrs || !next_l0_ptrs || !pts || !out_pos || !status))
+    return V2D_EINVAL;
+  if ((int64_t)B * P > 0 && levels > 1 && (!prev_pyr_ptrs || !next_pyr_ptrs)) return V2D_EINVAL;
+  if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
+  v2d::KltArgs a{W, H, P, win, iters, eps, ncc_min, min_eig, l0_pitch};
+  return v2d::launch_klt(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, B, lv, a, pts,
+                         guess, in_status, out_pos, status, ncc, iters_out,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

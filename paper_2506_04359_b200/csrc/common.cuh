@@ -1,0 +1,47 @@
+// common.cuh — internal helpers shared by the sm_100a kernels of the 2D hot path.
+// Product code only: nothing here is shared with oracle/ (task rule ③).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vslam2d.h"
+
+namespace v2d {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// Level geometry passed by value to kernels (mirrors v2d_layout).
+struct Levels {
+  int n;
+  int W[V2D_MAX_LEVELS];
+  int H[V2D_MAX_LEVELS];
+  int64_t pitch[V2D_MAX_LEVELS];   // floats (levels >= 1)
+  int64_t offset[V2D_MAX_LEVELS];  // floats (levels >= 1)
+};
+
+__host__ __device__ inline int64_t round_up64(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Launch helpers (defined in the kernel translation units).
+int launch_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
+                   const Levels& lv, float* const* pyr_ptrs, cudaStream_t st);
+
+struct GfttArgs {
+  int W, H, grid_x, grid_y, k, border, nms;
+  float min_score;
+  int64_t pitch;
+};
+int launch_gftt(const uint8_t* const* l0_ptrs, int B, const GfttArgs& a, float* kp_xy,
+                float* kp_score, int32_t* cell_count, float* resp, cudaStream_t st);
+
+struct KltArgs {
+  int W, H, P, win, iters;
+  float eps, ncc_min, min_eig;
+  int64_t l0_pitch;
+};
+int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
+               const uint8_t* const* next_l0, const float* const* next_pyr, int B,
+               const Levels& lv, const KltArgs& a, const float* pts, const float* guess,
+               const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
+               int32_t* iters_out, cudaStream_t st);
+
+}  // namespace v2d

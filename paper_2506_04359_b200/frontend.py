@@ -1,0 +1,126 @@
+"""Batched per-camera-frame pipeline over the C ABI.
+
+One *step* processes F consecutive frames of C cameras (B = F*C images, batch
+index b = f*C + c):
+
+    v2d_build_pyramid(frames t..t+F-1)                      -> pyr[parity]
+    v2d_detect_gftt  (frames t..t+F-1)                      -> kp slots 1..F
+    v2d_track_klt    (pyr_{t+f-1} -> pyr_{t+f}, pts = kp slots 0..F-1)
+    kp slot 0 <- kp slot F     (carry: frame t+F-1's keypoints feed the next step)
+
+Frames are addressed through device pointer tables, so a ring of rendered
+frames in HBM (bench `value`) and a two-slot staging buffer filled from pinned
+host memory (bench `e2e`) run the same three launches.  Nothing here computes
+any part of the method: it allocates, builds pointer tables and calls the ABI.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import vslam2d as v2d
+from .vslam2d import FrontendConfig
+
+
+class Frontend2D:
+    def __init__(self, cfg: FrontendConfig, cams: int, frames_per_step: int, device,
+                 l0_pitch: int):
+        self.cfg, self.C, self.F, self.dev = cfg, cams, frames_per_step, torch.device(device)
+        self.B = cams * frames_per_step
+        self.pitch = l0_pitch
+        self.layout = v2d.pyramid_layout(cfg.W, cfg.H, cfg.levels)
+        self.k = v2d.grid_k(cfg.grid_x, cfg.grid_y, cfg.k, cfg.K_min)
+        self.P = cfg.grid_x * cfg.grid_y * self.k
+        n = max(int(self.layout.floats_per_image), 32)
+        d = self.dev
+        # pyramids: two halves (step parity) x B images
+        self.pyr = torch.zeros((2, self.B, n), dtype=torch.float32, device=d)
+        # keypoints: slot j <-> frame t-1+j, each [C, P, 2] (batch order f*C + c)
+        self.kp_xy = torch.full((frames_per_step + 1, cams, self.P, 2), -1.0,
+                                dtype=torch.float32, device=d)
+        self.kp_score = torch.zeros((frames_per_step + 1, cams, self.P), dtype=torch.float32,
+                                    device=d)
+        self.cell_count = torch.zeros((frames_per_step + 1, cams, cfg.grid_x * cfg.grid_y),
+                                      dtype=torch.int32, device=d)
+        self.pos = torch.zeros((self.B, self.P, 2), dtype=torch.float32, device=d)
+        self.status = torch.zeros((self.B, self.P), dtype=torch.uint8, device=d)
+        self.ncc = torch.zeros((self.B, self.P), dtype=torch.float32, device=d)
+        self.iters = torch.zeros((self.B, self.P), dtype=torch.int32, device=d)
+        # pyramid pointer tables per parity: current and previous images
+        cur, prev = [], []
+        for par in (0, 1):
+            base = v2d.ptrs_of(self.pyr[par])
+            other = v2d.ptrs_of(self.pyr[1 - par])
+            cur.append(base)
+            pv = torch.empty_like(base)
+            pv[cams:] = base[:-cams]          # frame f-1 of this step
+            pv[:cams] = other[-cams:]         # last frame of the previous step
+            prev.append(pv)
+        self.pyr_ptrs, self.prev_pyr_ptrs = cur, prev
+        self.launches_per_step = 3
+
+    # ------------------------------------------------------------------
+    def step(self, l0_ptrs: torch.Tensor, prev_l0_ptrs: torch.Tensor, parity: int,
+             status_out: torch.Tensor | None = None, events=None):
+        """Enqueue one step.  l0_ptrs / prev_l0_ptrs: device int64 [B] pointer
+        tables of frames t+f and t+f-1 (batch order f*C + c).  `events`
+        (optional, 4 CUDA events) bracket the three launches for per-kernel
+        timing on the launching stream."""
+        c, B = self.cfg, self.B
+        W, H, L = c.W, c.H, c.levels
+        if events is not None:
+            events[0].record()
+        v2d.build_pyramid_ptrs(l0_ptrs, self.pitch, B, W, H, L, self.pyr_ptrs[parity])
+        if events is not None:
+            events[1].record()
+        v2d.detect_gftt_ptrs(l0_ptrs, self.pitch, B, W, H, c.grid_x, c.grid_y, c.k, c.K_min,
+                             c.min_score, c.border, c.nms, self.kp_xy[1:], self.kp_score[1:],
+                             self.cell_count[1:])
+        if events is not None:
+            events[2].record()
+        st = self.status if status_out is None else status_out
+        v2d.track_klt_ptrs(prev_l0_ptrs, self.prev_pyr_ptrs[parity], l0_ptrs,
+                           self.pyr_ptrs[parity], self.pitch, B, W, H, L, self.kp_xy[:-1],
+                           None, None, self.P, c.win, c.iters, c.eps, c.ncc_min, c.min_eig,
+                           self.pos, st, self.ncc, self.iters)
+        if events is not None:
+            events[3].record()
+        self.kp_xy[0].copy_(self.kp_xy[-1], non_blocking=True)
+
+    def prime(self, l0_ptrs_last: torch.Tensor, parity_prev: int):
+        """Fill the previous-frame state (pyramid of the frame before the first
+        step, and its keypoints) so step 0 tracks real data."""
+        c = self.cfg
+        C = self.C
+        pyr_ptrs = self.pyr_ptrs[parity_prev][-C:]
+        v2d.build_pyramid_ptrs(l0_ptrs_last, self.pitch, C, c.W, c.H, c.levels, pyr_ptrs)
+        v2d.detect_gftt_ptrs(l0_ptrs_last, self.pitch, C, c.W, c.H, c.grid_x, c.grid_y, c.k,
+                             c.K_min, c.min_score, c.border, c.nms, self.kp_xy[0],
+                             self.kp_score[0], self.cell_count[0])
+
+
+class RingSchedule:
+    """Pointer tables for stepping through a device ring frames[C, R, H, pitch]
+    F frames at a time (R must be a multiple of 2F so parity and ring index
+    advance together)."""
+
+    def __init__(self, frames: torch.Tensor, F: int):
+        C, R = frames.shape[0], frames.shape[1]
+        assert R % (2 * F) == 0, "ring length must be a multiple of 2F"
+        self.C, self.R, self.F = C, R, F
+        self.n_steps = R // F
+        img = frames.stride(1) * frames.element_size()
+        cam = frames.stride(0) * frames.element_size()
+        base = frames.data_ptr()
+        dev = frames.device
+        s = torch.arange(self.n_steps, device=dev, dtype=torch.int64)[:, None, None]
+        f = torch.arange(F, device=dev, dtype=torch.int64)[None, :, None]
+        c = torch.arange(C, device=dev, dtype=torch.int64)[None, None, :]
+        t = s * F + f
+        self.cur = (base + c * cam + (t % R) * img).reshape(self.n_steps, F * C).contiguous()
+        self.prev = (base + c * cam + ((t - 1) % R) * img).reshape(self.n_steps, F * C).contiguous()
+        last = (base + torch.arange(C, device=dev, dtype=torch.int64) * cam + (R - 1) * img)
+        self.before_first = last.contiguous()
+
+    def tables(self, step: int):
+        i = step % self.n_steps
+        return self.cur[i], self.prev[i], i % 2

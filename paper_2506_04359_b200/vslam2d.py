@@ -1,0 +1,221 @@
+"""Thin Python binding of the C ABI in include/vslam2d.h (ctypes).
+
+Argument marshalling only: every step of the path runs in the sm_100a kernels
+of libvslam2d.so.  There is no CPU fallback — importing this module on a box
+without the built library raises, and every call requires CUDA tensors.
+
+Function names mirror the C ABI (v2d_build_pyramid -> build_pyramid, ...).
+All calls are enqueued on torch.cuda.current_stream() and return without
+synchronising.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+TRACKED, LOST_OOB, LOST_NCC, LOST_SMALL_EIG, SKIPPED = 0, 1, 2, 3, 4
+MAX_LEVELS, MAX_K, MAX_WIN = 8, 256, 29
+
+
+class V2DError(RuntimeError):
+    pass
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int), ("W", ctypes.c_int * 8), ("H", ctypes.c_int * 8),
+                ("pitch", ctypes.c_int64 * 8), ("offset", ctypes.c_int64 * 8),
+                ("floats_per_image", ctypes.c_int64)]
+
+
+_SYMBOLS = ("v2d_pyramid_layout", "v2d_grid_k", "v2d_build_pyramid", "v2d_detect_gftt",
+            "v2d_track_klt", "v2d_strerror", "v2d_version")
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libvslam2d.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2506_04359_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i, i64, f = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
+    L.v2d_pyramid_layout.argtypes = [i, i, i, ctypes.POINTER(Layout)]
+    L.v2d_grid_k.argtypes = [i, i, i, i, ctypes.POINTER(ctypes.c_int)]
+    L.v2d_build_pyramid.argtypes = [vp, i64, i, i, i, i, vp, vp]
+    L.v2d_detect_gftt.argtypes = [vp, i64, i, i, i, i, i, i, i, f, i, i, vp, vp, vp, vp, vp]
+    L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
+                                vp, vp, vp, vp, vp]
+    L.v2d_strerror.argtypes = [i]
+    L.v2d_strerror.restype = ctypes.c_char_p
+    L.v2d_version.restype = i
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    L = load()
+    return [s for s in _SYMBOLS if hasattr(L, s)]
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise V2DError(f"{what}: {load().v2d_strerror(rc).decode()} (rc={rc})")
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise V2DError("vslam2d: tensors must live on a CUDA device (no CPU fallback)")
+
+
+# --------------------------------------------------------------------------
+# host helpers
+# --------------------------------------------------------------------------
+def pyramid_layout(W: int, H: int, levels: int) -> Layout:
+    out = Layout()
+    _check(load().v2d_pyramid_layout(W, H, levels, ctypes.byref(out)), "pyramid_layout")
+    return out
+
+
+def grid_k(grid_x: int, grid_y: int, k: int, K_min: int) -> int:
+    out = ctypes.c_int(0)
+    _check(load().v2d_grid_k(grid_x, grid_y, k, K_min, ctypes.byref(out)), "grid_k")
+    return out.value
+
+
+def ptrs_of(t: torch.Tensor) -> torch.Tensor:
+    """Device int64 array of per-image base pointers of a batched tensor
+    t[B, ...] (no host sync: computed on the device)."""
+    B = t.shape[0]
+    stride = t.stride(0) * t.element_size()
+    return t.data_ptr() + torch.arange(B, device=t.device, dtype=torch.int64) * stride
+
+
+def level_view(pyr: torch.Tensor, lay: Layout, L: int) -> torch.Tensor:
+    """[B, H_L, W_L] view of level L (>= 1) of batched pyramids pyr[B, floats]."""
+    off, pitch, w, h = lay.offset[L], lay.pitch[L], lay.W[L], lay.H[L]
+    return pyr[:, off:off + pitch * h].view(pyr.shape[0], h, pitch)[:, :, :w]
+
+
+# --------------------------------------------------------------------------
+# pointer-array entry points (1:1 with the C ABI)
+# --------------------------------------------------------------------------
+def build_pyramid_ptrs(l0_ptrs, l0_pitch, B, W, H, levels, pyr_ptrs):
+    _check(load().v2d_build_pyramid(_p(l0_ptrs), l0_pitch, B, W, H, levels, _p(pyr_ptrs),
+                                    _stream()), "build_pyramid")
+
+
+def detect_gftt_ptrs(l0_ptrs, l0_pitch, B, W, H, grid_x, grid_y, k, K_min, min_score, border,
+                     nms, kp_xy, kp_score, cell_count, resp=None):
+    _need_cuda(kp_xy, kp_score, cell_count, resp)
+    _check(load().v2d_detect_gftt(_p(l0_ptrs), l0_pitch, B, W, H, grid_x, grid_y, k, K_min,
+                                  float(min_score), border, nms, _p(kp_xy), _p(kp_score),
+                                  _p(cell_count), _p(resp), _stream()), "detect_gftt")
+
+
+def track_klt_ptrs(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, l0_pitch, B, W, H,
+                   levels, pts, guess, in_status, P, win, iters, eps, ncc_min, min_eig, out_pos,
+                   status, ncc=None, iters_out=None):
+    _need_cuda(pts, guess, in_status, out_pos, status, ncc, iters_out)
+    _check(load().v2d_track_klt(_p(prev_l0_ptrs), _p(prev_pyr_ptrs), _p(next_l0_ptrs),
+                                _p(next_pyr_ptrs), l0_pitch, B, W, H, levels, _p(pts), _p(guess),
+                                _p(in_status), P, win, iters, float(eps), float(ncc_min),
+                                float(min_eig), _p(out_pos), _p(status), _p(ncc), _p(iters_out),
+                                _stream()), "track_klt")
+
+
+# --------------------------------------------------------------------------
+# tensor-level conveniences
+# --------------------------------------------------------------------------
+def _frames(frames: torch.Tensor):
+    """frames: uint8 CUDA [B, H, pitch] (pitch % 16 == 0, contiguous rows)."""
+    _need_cuda(frames)
+    if frames.dtype != torch.uint8 or frames.dim() != 3 or frames.stride(2) != 1:
+        raise V2DError("frames must be uint8 [B, H, pitch] with unit column stride")
+    return frames.shape[0], frames.shape[1], frames.stride(1)
+
+
+def build_pyramid(frames: torch.Tensor, W: int, levels: int, out: torch.Tensor | None = None):
+    """Pyramids of B frames -> fp32 [B, floats_per_image] (levels 1..L-1)."""
+    B, H, pitch = _frames(frames)
+    lay = pyramid_layout(W, H, levels)
+    n = max(int(lay.floats_per_image), 32)
+    if out is None:
+        out = torch.empty((B, n), dtype=torch.float32, device=frames.device)
+    build_pyramid_ptrs(ptrs_of(frames), pitch, B, W, H, levels, ptrs_of(out))
+    return out
+
+
+def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int = 0,
+                K_min: int = 0, min_score: float = 0.0, border: int = 11, nms: int = 1,
+                want_resp: bool = False):
+    """-> (kp_xy [B,gy,gx,k,2], kp_score [B,gy,gx,k], cell_count [B,gy*gx], resp|None)."""
+    B, H, pitch = _frames(frames)
+    kk = grid_k(grid_x, grid_y, k, K_min)
+    dev = frames.device
+    xy = torch.empty((B, grid_y, grid_x, kk, 2), dtype=torch.float32, device=dev)
+    sc = torch.empty((B, grid_y, grid_x, kk), dtype=torch.float32, device=dev)
+    cnt = torch.empty((B, grid_y * grid_x), dtype=torch.int32, device=dev)
+    resp = torch.empty((B, H, W), dtype=torch.float32, device=dev) if want_resp else None
+    detect_gftt_ptrs(ptrs_of(frames), pitch, B, W, H, grid_x, grid_y, k, K_min, min_score,
+                     border, nms, xy, sc, cnt, resp)
+    return xy, sc, cnt, resp
+
+
+def track_klt(prev_frames, prev_pyr, next_frames, next_pyr, W: int, levels: int,
+              pts: torch.Tensor, guess=None, in_status=None, win: int = 21, iters: int = 10,
+              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01):
+    """pts [B, P, 2] -> (pos [B,P,2], status u8 [B,P], ncc [B,P], iters int32 [B,P])."""
+    B, H, pitch = _frames(prev_frames)
+    _frames(next_frames)
+    P = pts.shape[1]
+    dev = pts.device
+    pts = pts.contiguous().float()
+    pos = torch.empty((B, P, 2), dtype=torch.float32, device=dev)
+    st = torch.empty((B, P), dtype=torch.uint8, device=dev)
+    nc = torch.empty((B, P), dtype=torch.float32, device=dev)
+    it = torch.empty((B, P), dtype=torch.int32, device=dev)
+    track_klt_ptrs(ptrs_of(prev_frames), ptrs_of(prev_pyr), ptrs_of(next_frames),
+                   ptrs_of(next_pyr), pitch, B, W, H, levels, pts,
+                   None if guess is None else guess.contiguous().float(),
+                   None if in_status is None else in_status.contiguous(), P, win, iters, eps,
+                   ncc_min, min_eig, pos, st, nc, it)
+    return pos, st, nc, it
+
+
+@dataclass
+class FrontendConfig:
+    W: int
+    H: int
+    levels: int
+    grid_x: int = 8
+    grid_y: int = 8
+    k: int = 0
+    K_min: int = 0
+    min_score: float = 0.0
+    border: int = 11
+    nms: int = 1
+    win: int = 21
+    iters: int = 10
+    eps: float = 0.01
+    ncc_min: float = 0.8
+    min_eig: float = 0.01

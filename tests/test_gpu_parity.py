@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same
+seeded bytes, element by element.  Bars: pyramid, response and
+selection bit-exact; KLT positions <= 0.01 px for slots tracked on both sides
+and identical status except rounding-attributable flips inside the stated
+bands (tests/parity.py)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.parity import compare_klt, gpu_level_planes
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2506_04359_b200 import vslam2d as v2d
+
+
+def _to_dev(frames_u8: np.ndarray, pitch: int | None = None):
+    """[B, H, W] host u8 -> [B, H, pitch] device (pitch % 16 == 0)."""
+    B, H, W = frames_u8.shape
+    pitch = pitch or synth.round_up(W, 16)
+    t = torch.zeros((B, H, pitch), dtype=torch.uint8)
+    t[:, :, :W] = torch.from_numpy(frames_u8)
+    return t.cuda()
+
+
+def _stream(W, H, n, seed, motion=(3.0, 2.0)):
+    wl = synth.Workload("t", 7, W, H, 1, 3, motion=motion)
+    st = synth.make_stream(wl, n, "cpu", rank_salt=seed)
+    return st.frames[0][:, :, :W].numpy().copy(), st
+
+
+# ------------------------------------------------------------------ pyramid
+@pytest.mark.parametrize("W,H,levels", [(640, 480, 3), (752, 480, 4), (1241, 376, 4),
+                                        (155, 47, 4), (33, 17, 5), (300, 260, 8), (64, 64, 1),
+                                        (1, 1, 1), (129, 2, 2)])
+def test_pyramid_bit_exact(W, H, levels):
+    rng = np.random.default_rng(W * 7 + H)
+    fr = rng.integers(0, 256, (3, H, W), dtype=np.uint8)
+    d = _to_dev(fr)
+    pyr = v2d.build_pyramid(d, W, levels).cpu().numpy()
+    lay = v2d.pyramid_layout(W, H, levels)
+    for b in range(3):
+        planes, _ = oracle.build_pyramid(fr[b], levels)
+        got = gpu_level_planes(pyr[b], lay, levels)
+        for L in range(1, levels):
+            assert np.array_equal(got[L - 1].astype(np.float64), planes[L]), (b, L)
+
+
+def test_pyramid_unaligned_pitch_rejected():
+    d = torch.zeros((1, 10, 40), dtype=torch.uint8, device="cuda")
+    with pytest.raises(v2d.V2DError):
+        v2d.build_pyramid(d, 33, 2)  # pitch 40 % 16 != 0
+
+
+# ---------------------------------------------------------- response/select
+@pytest.mark.parametrize("W,H,seed", [(160, 120, 0), (97, 61, 1), (752, 480, 2)])
+def test_response_bit_exact(W, H, seed):
+    fr, _ = _stream(W, H, 2, seed)
+    d = _to_dev(fr)
+    _, _, _, resp = v2d.detect_gftt(d, W, 4, 3, k=8, border=3, want_resp=True)
+    resp = resp.cpu().numpy()
+    for b in range(fr.shape[0]):
+        R, _ = oracle.response(fr[b])
+        assert np.array_equal(resp[b], R)
+
+
+SELECT_CASES = [
+    # W, H, gx, gy, k, K_min, border, nms, min_score
+    (640, 480, 8, 8, 4, 200, 11, 1, 0.0),
+    (752, 480, 8, 8, 0, 1000, 11, 1, 0.0),
+    (1241, 376, 8, 8, 0, 2000, 11, 1, 0.0),
+    (97, 61, 3, 2, 7, 0, 3, 1, 0.0),
+    (97, 61, 3, 2, 7, 0, 3, 0, 0.0),
+    (200, 150, 2, 2, 256, 0, 5, 1, 0.0),
+    (200, 150, 1, 1, 256, 0, 3, 0, 0.0),
+    (333, 111, 7, 5, 3, 0, 11, 1, 50.0),
+]
+
+
+@pytest.mark.parametrize("W,H,gx,gy,k,K,border,nms,ms", SELECT_CASES)
+def test_selection_bit_exact(W, H, gx, gy, k, K, border, nms, ms):
+    fr, _ = _stream(W, H, 3, W + H)
+    d = _to_dev(fr)
+    xy, sc, cnt, _ = v2d.detect_gftt(d, W, gx, gy, k=k, K_min=K, border=border, nms=nms,
+                                     min_score=ms)
+    xy, sc, cnt = xy.cpu().numpy(), sc.cpu().numpy(), cnt.cpu().numpy()
+    for b in range(fr.shape[0]):
+        oxy, osc, ocnt = oracle.detect_gftt(fr[b], gx, gy, k=k, K_min=K, min_score=ms,
+                                            border=border, nms=nms)
+        assert np.array_equal(cnt[b], ocnt)
+        assert np.array_equal(xy[b], oxy)
+        assert np.array_equal(sc[b], osc)
+
+
+def test_selection_special_images():
+    W, H = 128, 96
+    const = np.full((H, W), 90, np.uint8)
+    tile = np.zeros((8, 8), np.uint8)
+    tile[2:6, 2:6] = 200
+    ties = np.tile(tile, (H // 8, W // 8))
+    corner = np.full((H, W), 40, np.uint8)
+    corner[50:, 70:] = 220
+    fr = np.stack([const, ties, corner])
+    d = _to_dev(fr)
+    xy, sc, cnt, _ = v2d.detect_gftt(d, W, 2, 2, k=40, border=3)
+    for b in range(3):
+        oxy, osc, ocnt = oracle.detect_gftt(fr[b], 2, 2, k=40, border=3)
+        assert np.array_equal(xy[b].cpu().numpy(), oxy)
+        assert np.array_equal(sc[b].cpu().numpy(), osc)
+        assert np.array_equal(cnt[b].cpu().numpy(), ocnt)
+    assert cnt[0].sum().item() == 0
+
+
+def test_detect_rejects_bad_k():
+    d = torch.zeros((1, 64, 64), dtype=torch.uint8, device="cuda")
+    with pytest.raises(v2d.V2DError):
+        v2d.detect_gftt(d, 64, 8, 8, k=4, K_min=256, border=3)  # violates Eq. 1
+
+
+# ---------------------------------------------------------------------- KLT
+def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in_status=None,
+              eps=0.01):
+    B = fr_prev.shape[0]
+    dp, dn = _to_dev(fr_prev), _to_dev(fr_next)
+    pp = v2d.build_pyramid(dp, W, levels)
+    pn = v2d.build_pyramid(dn, W, levels)
+    tp = torch.from_numpy(pts).cuda()
+    tg = None if guess is None else torch.from_numpy(guess).cuda()
+    ti = None if in_status is None else torch.from_numpy(in_status).cuda()
+    pos, st, nc, it = v2d.track_klt(dp, pp, dn, pn, W, levels, tp, guess=tg, in_status=ti,
+                                    win=win, iters=iters, eps=eps)
+    pos, st, nc = pos.cpu().numpy(), st.cpu().numpy(), nc.cpu().numpy()
+    H = fr_prev.shape[1]
+    stats = []
+    for b in range(B):
+        _, d0 = oracle.build_pyramid(fr_prev[b], levels)
+        _, d1 = oracle.build_pyramid(fr_next[b], levels)
+        opos, ost, onc, dg = oracle.track_klt(
+            d0, d1, W, H, levels, pts[b], guess=None if guess is None else guess[b],
+            in_status=None if in_status is None else in_status[b], win=win, iters=iters, eps=eps)
+        stats.append(compare_klt(pts[b], pos[b], st[b], opos, ost, dg))
+    return stats
+
+
+def test_klt_c1_pair():
+    """BASELINE config C1: 640x480, 3 levels, 8x8 grid, k=4, 21x21 window."""
+    f0, f1 = synth.shifted_pair(480, 640, (3.2, -1.7), seed=1)
+    xy, _, _ = oracle.detect_gftt(f0, 8, 8, k=4, K_min=200, border=11)
+    pts = xy.reshape(1, -1, 2)
+    stats = _klt_case(f0[None], f1[None], 640, 3, pts)
+    assert stats[0]["both_tracked"] > 200
+    assert stats[0]["max_pos_err"] <= 0.01
+
+
+@pytest.mark.parametrize("win,levels", [(21, 4), (11, 3), (29, 2), (3, 1), (7, 5)])
+def test_klt_stream_windows(win, levels):
+    W, H = 320, 240
+    fr, _ = _stream(W, H, 4, 11 + win, motion=(4.0, 3.0))
+    prev, nxt = fr[:-1], fr[1:]
+    pts = np.stack([oracle.detect_gftt(f, 4, 4, k=16, border=(win - 1) // 2 + 1)[0].reshape(-1, 2)
+                    for f in prev])
+    stats = _klt_case(prev, nxt, W, levels, pts, win=win)
+    assert sum(s["both_tracked"] for s in stats) > 0.3 * pts.shape[0] * pts.shape[1]
+
+
+def test_klt_edge_cases():
+    W, H = 200, 150
+    fr, _ = _stream(W, H, 2, 5)
+    pts = np.array([[[-1, -1], [100, 70], [12, 12], [187, 137], [3, 75], [199, 149],
+                     [60.25, 40.75], [150, 20], [np.nan, 3], [0, 0]]], np.float32)
+    ins = np.array([[0, 1, 0, 0, 0, 0, 0, 0, 0, 0]], np.uint8)
+    guess = np.tile(np.array([[[2.5, -1.0]]], np.float32), (1, pts.shape[1], 1))
+    _klt_case(fr[:1], fr[1:], W, 3, pts, in_status=ins)
+    _klt_case(fr[:1], fr[1:], W, 3, pts, guess=guess)
+    # identical frames: zero motion exactly
+    d = _to_dev(fr[:1])
+    p = v2d.build_pyramid(d, W, 3)
+    good = torch.tensor([[[100.0, 70.0], [60.0, 41.0]]], device="cuda")
+    pos, st, nc, it = v2d.track_klt(d, p, d, p, W, 3, good)
+    assert st.tolist() == [[0, 0]]
+    assert torch.equal(pos, good)
+
+
+def test_klt_noise_rejects():
+    W, H = 320, 240
+    fr, _ = _stream(W, H, 1, 3)
+    noise = synth.noise_frame(H, W, 99)[None]
+    pts = oracle.detect_gftt(fr[0], 4, 4, k=8, border=11)[0].reshape(1, -1, 2)
+    stats = _klt_case(fr, noise, W, 3, pts)
+    valid = (pts[0, :, 0] >= 0).sum()
+    assert stats[0]["status_hist_gpu"][0] <= 0.1 * valid
