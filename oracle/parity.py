@@ -1,5 +1,7 @@
-"""Helpers shared by the GPU parity tests: run the oracle on the same bytes
-and compare element by element (SURVEY §8(c) "Tolerances")."""
+"""TEST INFRASTRUCTURE (oracle side): element-by-element comparison of
+CUDA-path outputs with the oracle run on the same bytes, used by tests/ and
+__graft_entry__.smoke().  Tolerances and ambiguity bands: SURVEY §8(c)
+"Tolerances", DESIGN.md §3."""
 from __future__ import annotations
 
 import numpy as np

@@ -359,6 +359,8 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
         !isfinite(py)) {
       st = V2DREF_SKIPPED;
     }
+    if (st == V2DREF_TRACKED && (px < 0.0 || px > W - 1 || py < 0.0 || py > H - 1))
+      st = V2DREF_LOST_OOB; /* reading #16: a start point outside the image is lost */
     double dx = 0.0, dy = 0.0;
     if (st == V2DREF_TRACKED && guess) {
       dx = guess[2 * p] / (double)(1 << (levels - 1));

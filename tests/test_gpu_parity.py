@@ -2,14 +2,14 @@
 seeded bytes, element by element.  Bars: pyramid, response and
 selection bit-exact; KLT positions <= 0.01 px for slots tracked on both sides
 and identical status except rounding-attributable flips inside the stated
-bands (tests/parity.py)."""
+bands (oracle/parity.py)."""
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import synth
-from tests.parity import compare_klt, gpu_level_planes
+from oracle.parity import compare_klt, gpu_level_planes
 
 pytestmark = pytest.mark.gpu
 
@@ -160,7 +160,7 @@ def test_klt_stream_windows(win, levels):
     W, H = 320, 240
     fr, _ = _stream(W, H, 4, 11 + win, motion=(4.0, 3.0))
     prev, nxt = fr[:-1], fr[1:]
-    pts = np.stack([oracle.detect_gftt(f, 4, 4, k=16, border=(win - 1) // 2 + 1)[0].reshape(-1, 2)
+    pts = np.stack([oracle.detect_gftt(f, 4, 4, k=16, border=max(3, (win - 1) // 2 + 1))[0].reshape(-1, 2)
                     for f in prev])
     stats = _klt_case(prev, nxt, W, levels, pts, win=win)
     assert sum(s["both_tracked"] for s in stats) > 0.3 * pts.shape[0] * pts.shape[1]
