@@ -32,13 +32,22 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kPitch = 32;                 // smem patch row pitch (floats)
-constexpr int kPatch = 32 * kPitch;        // floats per warp
+constexpr int kPitch = 32;  // smem row pitch (floats); lane = column
+
+// Per-warp shared memory: one 32x32 patch (template source, then the next-level
+// search patch) + the two (WIN+1)-row gradient grids of the template.
+template <int WIN>
+struct Smem {
+  static constexpr int PATCH = 32 * kPitch;
+  static constexpr int GRID = (WIN + 1) * kPitch;
+  static constexpr int TOTAL = PATCH + 2 * GRID;
+};
 
 struct Plane {
   const void* base;
   int64_t pitch;  // elements
   int W, H;
+  int u8;         // 1: uint8 L0 frame, 0: fp32 pyramid level
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
@@ -49,6 +58,7 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 __device__ __forceinline__ float2 warp_sum2(float2 v) {
 #pragma unroll
@@ -60,19 +70,27 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
   return v;
 }
 
-// Stage rows [oy, oy+NR) x columns [ox, ox+32) of a level (clamp-to-edge) into
-// the warp's patch, minus `shift`; lane = column.
-template <typename TI, int NR>
+// Stage rows [oy, oy+nrows) x columns [ox, ox+32) of a level (clamp-to-edge)
+// into a warp patch, minus `shift` (lane = column).
 __device__ __forceinline__ void stage(float* __restrict__ sp, const Plane& pl, int ox, int oy,
-                                      float shift) {
+                                      int nrows, float shift) {
   const int lane = threadIdx.x & 31;
-  const TI* __restrict__ col =
-      reinterpret_cast<const TI*>(pl.base) + clampi(ox + lane, 0, pl.W - 1);
+  const int x = clampi(ox + lane, 0, pl.W - 1);
   __syncwarp();
-#pragma unroll 8
-  for (int r = 0; r < NR; ++r) {
-    const int y = clampi(oy + r, 0, pl.H - 1);
-    sp[r * kPitch + lane] = (float)__ldg(col + (int64_t)y * pl.pitch) - shift;
+  if (pl.u8) {
+    const uint8_t* __restrict__ col = reinterpret_cast<const uint8_t*>(pl.base) + x;
+#pragma unroll 4
+    for (int r = 0; r < nrows; ++r) {
+      const int y = clampi(oy + r, 0, pl.H - 1);
+      sp[r * kPitch + lane] = (float)__ldg(col + (int64_t)y * pl.pitch) - shift;
+    }
+  } else {
+    const float* __restrict__ col = reinterpret_cast<const float*>(pl.base) + x;
+#pragma unroll 4
+    for (int r = 0; r < nrows; ++r) {
+      const int y = clampi(oy + r, 0, pl.H - 1);
+      sp[r * kPitch + lane] = __ldg(col + (int64_t)y * pl.pitch) - shift;
+    }
   }
   __syncwarp();
 }
@@ -84,222 +102,182 @@ struct LevelOut {
   int levels;  // levels whose template was built
 };
 
+// Template rows in split pairs: .x = window row p, .y = window row p + H2 - 1
+// (H2 = (WIN+1)/2); the y-copy of the shared middle row (p = 0) is zeroed.
 template <int WIN>
 struct Tmpl {
-  static constexpr int NPAIR = WIN / 2;  // row pairs; WIN odd -> one tail row
-  float2 T[NPAIR], TX[NPAIR], TY[NPAIR];
-  float Tt, TXt, TYt;                    // tail row WIN-1
-  // row v (compile-time after unrolling) of each quantity
-  __device__ __forceinline__ void set(int v, float tv, float txv, float tyv) {
-    if (v == WIN - 1) {
-      Tt = tv;
-      TXt = txv;
-      TYt = tyv;
-    } else if (v & 1) {
-      T[v >> 1].y = tv;
-      TX[v >> 1].y = txv;
-      TY[v >> 1].y = tyv;
-    } else {
-      T[v >> 1].x = tv;
-      TX[v >> 1].x = txv;
-      TY[v >> 1].x = tyv;
-    }
-  }
+  static constexpr int H2 = (WIN + 1) / 2;
+  float2 T[H2], TX[H2], TY[H2];
 };
 
-// Template of D7 at level L from the staged previous-level patch P
-// (P[r][c] = I~(px0 + c, py0 + r), px0 = ix-R-1, py0 = iy-R-1).
+// D7 template at one level from the staged previous-level patch P
+// (P[r][c] = I~(ix-R-1+c, iy-R-1+r)).  Gradient grids GX/GY (grid point
+// (c, g) <-> pixel (ix-R+c, iy-R+g)) hold the clamp-to-edge Sobel/8 gradient
+// IMAGE sampled with clamped coordinates, exactly as the oracle samples it.
 template <int WIN>
-__device__ __forceinline__ void build_template(const float* __restrict__ P, int ix, int iy,
-                                               float ax, float ay, int W, int H, Tmpl<WIN>& t) {
+__device__ __forceinline__ void build_template(const float* __restrict__ P,
+                                               float* __restrict__ GX, float* __restrict__ GY,
+                                               int ix, int iy, float ax, float ay, int W, int H,
+                                               Tmpl<WIN>& t) {
   constexpr int R = (WIN - 1) / 2;
+  constexpr int H2 = Tmpl<WIN>::H2;
   const int lane = threadIdx.x & 31;
-  const int i = min(lane, WIN);  // grid column of this lane (lanes > WIN duplicate WIN)
-  const bool interior = (ix - R >= 0) && (ix + R + 1 <= W - 1) && (iy - R >= 0) &&
-                        (iy + R + 1 <= H - 1);
-  if (interior) {
-    // rolling 3x3 over patch rows; grid row g = r-2 centred at patch row r-1
-    float L1 = 0.f, L2 = 0.f, C1 = 0.f, C2 = 0.f, R1 = 0.f, R2 = 0.f;
-    float hp_prev = 0.f, hgx_prev = 0.f, hgy_prev = 0.f, tpend = 0.f;
-#pragma unroll
-    for (int r = 0; r < WIN + 3; ++r) {
-      const float* row = P + r * kPitch;
-      const float l = row[i], c = row[i + 1], rr = row[i + 2];
-      const float hp = fmaf(ax, rr - c, c);
-      if (r >= 2) {
-        const float tnew = fmaf(ay, hp - hp_prev, hp_prev);  // T row r-2
-        const float2 V = fma2(f2(2.f, 2.f), f2(L1, R1), add2(f2(L2, R2), f2(l, rr)));
-        const float gx = (V.y - V.x) * 0.125f;
-        const float gy = ((l - L2) + 2.f * (c - C2) + (rr - R2)) * 0.125f;
-        const float gx1 = __shfl_down_sync(kFullMask, gx, 1);
-        const float gy1 = __shfl_down_sync(kFullMask, gy, 1);
-        const float2 hg = fma2(f2(ax, ax), sub2(f2(gx1, gy1), f2(gx, gy)), f2(gx, gy));
-        const int g = r - 2;
-        if (g >= 1) {
-          const float2 tg = fma2(f2(ay, ay), sub2(hg, f2(hgx_prev, hgy_prev)),
-                                 f2(hgx_prev, hgy_prev));
-          t.set(g - 1, tpend, tg.x, tg.y);
-        }
-        hgx_prev = hg.x;
-        hgy_prev = hg.y;
-        tpend = tnew;
-      }
-      hp_prev = hp;
-      L2 = L1; L1 = l;
-      C2 = C1; C1 = c;
-      R2 = R1; R1 = rr;
+  const int c = min(lane, WIN);
+  if ((ix - R >= 0) && (ix + R + 1 <= W - 1) && (iy - R >= 0) && (iy + R + 1 <= H - 1)) {
+    // every grid centre inside the image: rolling 3x3 Sobel over patch rows
+    float l0 = P[c], m0 = P[c + 1], r0 = P[c + 2];
+    float l1 = P[kPitch + c], m1 = P[kPitch + c + 1], r1 = P[kPitch + c + 2];
+#pragma unroll 2
+    for (int g = 0; g <= WIN; ++g) {
+      const float* row = P + (g + 2) * kPitch;
+      const float l2 = row[c], m2 = row[c + 1], r2 = row[c + 2];
+      GX[g * kPitch + lane] = ((r0 + 2.f * r1 + r2) - (l0 + 2.f * l1 + l2)) * 0.125f;
+      GY[g * kPitch + lane] = ((l2 + 2.f * m2 + r2) - (l0 + 2.f * m0 + r0)) * 0.125f;
+      l0 = l1; m0 = m1; r0 = r1;
+      l1 = l2; m1 = m2; r1 = r2;
     }
   } else {
-    // generic: gradients at clamped centres (the gradient IMAGE is clamped),
-    // intensities from the clamped patch
-    const int lc = clampi(ix - R + i, 0, W - 1) - (ix - R - 1);
-    float hp_prev = 0.f, hgx_prev = 0.f, hgy_prev = 0.f;
-#pragma unroll
+    // near a border: gradient at the clamped centre
+    const int lc = clampi(ix - R + c, 0, W - 1) - (ix - R - 1);
     for (int g = 0; g <= WIN; ++g) {
       const int lr = clampi(iy - R + g, 0, H - 1) - (iy - R - 1);
       const float* up = P + (lr - 1) * kPitch;
       const float* md = P + lr * kPitch;
       const float* dn = P + (lr + 1) * kPitch;
-      const float gx = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
-                        (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1])) * 0.125f;
-      const float gy = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
-                        (up[lc - 1] + 2.f * up[lc] + up[lc + 1])) * 0.125f;
-      const float* prow = P + (g + 1) * kPitch;  // T rows use patch rows g+1 (and g+2)
-      const float hp = fmaf(ax, prow[i + 2] - prow[i + 1], prow[i + 1]);
-      const float gx1 = __shfl_down_sync(kFullMask, gx, 1);
-      const float gy1 = __shfl_down_sync(kFullMask, gy, 1);
-      const float2 hg = fma2(f2(ax, ax), sub2(f2(gx1, gy1), f2(gx, gy)), f2(gx, gy));
-      if (g >= 1) {
-        const float2 tg = fma2(f2(ay, ay), sub2(hg, f2(hgx_prev, hgy_prev)),
-                               f2(hgx_prev, hgy_prev));
-        t.set(g - 1, fmaf(ay, hp - hp_prev, hp_prev), tg.x, tg.y);
-      }
-      hgx_prev = hg.x;
-      hgy_prev = hg.y;
-      hp_prev = hp;
+      GX[g * kPitch + lane] = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
+                               (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1])) * 0.125f;
+      GY[g * kPitch + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
+                               (up[lc - 1] + 2.f * up[lc] + up[lc + 1])) * 0.125f;
     }
+  }
+  __syncwarp();
+  // bilinear samples (shared weights ax, ay): T row v from patch rows v+1, v+2 /
+  // cols u+1, u+2; Tx, Ty row v from grid rows v, v+1 / cols u, u+1.
+  const int u = min(lane, WIN - 1);
+  const float2 wx = f2(ax, ax), wy = f2(ay, ay);
+  auto hrow = [&](const float* base, int ra, int rb, int col) {
+    const float2 a0 = f2(base[ra * kPitch + col], base[rb * kPitch + col]);
+    const float2 a1 = f2(base[ra * kPitch + col + 1], base[rb * kPitch + col + 1]);
+    return fma2(wx, sub2(a1, a0), a0);
+  };
+  float2 hp = hrow(P, 1, H2, u + 1);
+  float2 hx = hrow(GX, 0, H2 - 1, u);
+  float2 hy = hrow(GY, 0, H2 - 1, u);
+#pragma unroll
+  for (int p = 0; p < H2; ++p) {
+    const float2 np = hrow(P, p + 2, p + H2 + 1, u + 1);
+    const float2 nx = hrow(GX, p + 1, p + H2, u);
+    const float2 ny = hrow(GY, p + 1, p + H2, u);
+    t.T[p] = fma2(wy, sub2(np, hp), hp);
+    t.TX[p] = fma2(wy, sub2(nx, hx), hx);
+    t.TY[p] = fma2(wy, sub2(ny, hy), hy);
+    hp = np;
+    hx = nx;
+    hy = ny;
   }
   const float valid = lane < WIN ? 1.0f : 0.0f;
   const float2 vv = f2(valid, valid);
 #pragma unroll
-  for (int p = 0; p < Tmpl<WIN>::NPAIR; ++p) {
-    t.T[p] = __fmul2_rn(t.T[p], vv);
-    t.TX[p] = __fmul2_rn(t.TX[p], vv);
-    t.TY[p] = __fmul2_rn(t.TY[p], vv);
+  for (int p = 0; p < H2; ++p) {
+    const float2 m = p == 0 ? f2(valid, 0.f) : vv;
+    t.T[p] = mul2(t.T[p], m);
+    t.TX[p] = mul2(t.TX[p], m);
+    t.TY[p] = mul2(t.TY[p], m);
   }
-  t.Tt *= valid;
-  t.TXt *= valid;
-  t.TYt *= valid;
 }
 
-// Horizontal lerp of patch rows; S'(u, v) sampled at patch origin (lc0, lr0).
-// Returns sum over the window of e*(Tx, Ty) with e = T' - S' (both centred).
+// sum over the window of e*(Tx, Ty), e = T' - S' (S' bilinear of the centred,
+// staged next-level patch at origin (lc0, lr0) with weights (bx, by)).
 template <int WIN>
 __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, int lr0, float bx,
                                          float by, const Tmpl<WIN>& t) {
+  constexpr int H2 = Tmpl<WIN>::H2;
   const int lane = threadIdx.x & 31;
-  const int u = min(lane, WIN - 1);
-  const float* base = JP + lr0 * kPitch + lc0 + u;
+  const float* base = JP + lr0 * kPitch + lc0 + min(lane, WIN - 1);
   const float2 wx = f2(bx, bx), wy = f2(by, by);
-  float h0 = fmaf(bx, base[1] - base[0], base[0]);
+  auto hrow = [&](int ra, int rb) {
+    const float2 a0 = f2(base[ra * kPitch], base[rb * kPitch]);
+    const float2 a1 = f2(base[ra * kPitch + 1], base[rb * kPitch + 1]);
+    return fma2(wx, sub2(a1, a0), a0);
+  };
+  float2 h = hrow(0, H2 - 1);
   float2 ax = f2(0.f, 0.f), ay = f2(0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < Tmpl<WIN>::NPAIR; ++p) {
-    const float* r1 = base + (2 * p + 1) * kPitch;
-    const float* r2 = base + (2 * p + 2) * kPitch;
-    const float2 ja = f2(r1[0], r2[0]), jb = f2(r1[1], r2[1]);
-    const float2 h = fma2(wx, sub2(jb, ja), ja);                 // rows 2p+1, 2p+2
-    const float2 hv = f2(h0, h.x);                                // rows 2p, 2p+1
-    const float2 S = fma2(wy, sub2(h, hv), hv);                  // samples 2p, 2p+1
-    const float2 e = sub2(t.T[p], S);
+  for (int p = 0; p < H2; ++p) {
+    const float2 hn = hrow(p + 1, p + H2);
+    const float2 e = sub2(t.T[p], fma2(wy, sub2(hn, h), h));
     ax = fma2(e, t.TX[p], ax);
     ay = fma2(e, t.TY[p], ay);
-    h0 = h.y;
+    h = hn;
   }
-  float sx = ax.x + ax.y, sy = ay.x + ay.y;
-  {
-    const float* r = base + WIN * kPitch;
-    const float h = fmaf(bx, r[1] - r[0], r[0]);
-    const float e = t.Tt - fmaf(by, h - h0, h0);
-    sx = fmaf(e, t.TXt, sx);
-    sy = fmaf(e, t.TYt, sy);
-  }
-  return f2(sx, sy);
+  return f2(ax.x + ax.y, ay.x + ay.y);
 }
 
-// NCC moments of the centred patch: returns (sum S', sum S'^2, sum T'S').
+// NCC moments (sum S', sum S'^2, sum T'S') of the centred patches.
 template <int WIN>
 __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int lc0, int lr0,
                                               float bx, float by, const Tmpl<WIN>& t) {
+  constexpr int H2 = Tmpl<WIN>::H2;
   const int lane = threadIdx.x & 31;
-  const int u = min(lane, WIN - 1);
   const float valid = lane < WIN ? 1.0f : 0.0f;
-  const float* base = JP + lr0 * kPitch + lc0 + u;
-  const float2 wx = f2(bx, bx), wy = f2(by, by), vv = f2(valid, valid);
-  float h0 = fmaf(bx, base[1] - base[0], base[0]);
+  const float* base = JP + lr0 * kPitch + lc0 + min(lane, WIN - 1);
+  const float2 wx = f2(bx, bx), wy = f2(by, by);
+  auto hrow = [&](int ra, int rb) {
+    const float2 a0 = f2(base[ra * kPitch], base[rb * kPitch]);
+    const float2 a1 = f2(base[ra * kPitch + 1], base[rb * kPitch + 1]);
+    return fma2(wx, sub2(a1, a0), a0);
+  };
+  float2 h = hrow(0, H2 - 1);
   float2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f), st = f2(0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < Tmpl<WIN>::NPAIR; ++p) {
-    const float* r1 = base + (2 * p + 1) * kPitch;
-    const float* r2 = base + (2 * p + 2) * kPitch;
-    const float2 ja = f2(r1[0], r2[0]), jb = f2(r1[1], r2[1]);
-    const float2 h = fma2(wx, sub2(jb, ja), ja);
-    const float2 hv = f2(h0, h.x);
-    const float2 S = __fmul2_rn(fma2(wy, sub2(h, hv), hv), vv);
+  for (int p = 0; p < H2; ++p) {
+    const float2 hn = hrow(p + 1, p + H2);
+    const float2 m = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
+    const float2 S = mul2(fma2(wy, sub2(hn, h), h), m);
     s1 = add2(s1, S);
     s2 = fma2(S, S, s2);
     st = fma2(t.T[p], S, st);
-    h0 = h.y;
+    h = hn;
   }
-  float a = s1.x + s1.y, b = s2.x + s2.y, c = st.x + st.y;
-  {
-    const float* r = base + WIN * kPitch;
-    const float h = fmaf(bx, r[1] - r[0], r[0]);
-    const float S = fmaf(by, h - h0, h0) * valid;
-    a += S;
-    b = fmaf(S, S, b);
-    c = fmaf(t.Tt, S, c);
-  }
-  return make_float3(a, b, c);
+  return make_float3(s1.x + s1.y, s2.x + s2.y, st.x + st.y);
 }
 
-// One pyramid level of D7 for the warp's keypoint.
-template <int WIN, typename TI, typename TJ>
-__device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane& I, const Plane& J,
-                                            const int L, const double cx, const double cy,
-                                            double& dx, double& dy, const KltArgs& a,
-                                            LevelOut& out) {
+// One pyramid level of D7 for the warp's keypoint; (dx, dy) in level px.
+template <int WIN>
+__device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
+                                         const int L, const float cx, const float cy, float& dx,
+                                         float& dy, const KltArgs a, LevelOut& out) {
   constexpr int R = (WIN - 1) / 2;
   constexpr int N = WIN * WIN;
-  constexpr int M = (31 - WIN) / 2;        // staged motion margin (px)
-  constexpr int SZ = WIN + 1 + 2 * M;      // staged J patch edge (<= 32)
+  constexpr int M = (31 - WIN) / 2;    // staged motion margin (px)
+  constexpr int SZ = WIN + 1 + 2 * M;  // staged search patch edge (<= 32)
+  constexpr int H2 = Tmpl<WIN>::H2;
   static_assert(WIN + 3 <= 32 && SZ <= 32, "window too large for one warp");
   const int lane = threadIdx.x & 31;
+  float* GX = sp + Smem<WIN>::PATCH;
+  float* GY = GX + Smem<WIN>::GRID;
 
   // ---------------- template (previous frame) -----------------------------
   Tmpl<WIN> t;
   {
-    const double fcx = floor(cx), fcy = floor(cy);
+    const float fcx = floorf(cx), fcy = floorf(cy);
     const int ix = (int)fcx, iy = (int)fcy;
-    stage<TI, WIN + 3>(sp, I, ix - R - 1, iy - R - 1, 0.0f);
-    build_template<WIN>(sp, ix, iy, (float)(cx - fcx), (float)(cy - fcy), I.W, I.H, t);
+    stage(sp, I, ix - R - 1, iy - R - 1, WIN + 3, 0.0f);
+    build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, t);
   }
   out.levels++;
-  // G and template mean
-  float2 gxx_gxy = f2(0.f, 0.f), gyy_st = f2(0.f, 0.f);
+  float2 g01 = f2(0.f, 0.f), g2s = f2(0.f, 0.f);  // (Gxx, Gxy), (Gyy, sum T)
 #pragma unroll
-  for (int p = 0; p < Tmpl<WIN>::NPAIR; ++p) {
+  for (int p = 0; p < H2; ++p) {
     const float2 tx = t.TX[p], ty = t.TY[p], tt = t.T[p];
-    gxx_gxy = fma2(f2(tx.x, tx.x), f2(tx.x, ty.x), gxx_gxy);
-    gxx_gxy = fma2(f2(tx.y, tx.y), f2(tx.y, ty.y), gxx_gxy);
-    gyy_st = fma2(f2(ty.x, 1.f), f2(ty.x, tt.x), gyy_st);
-    gyy_st = fma2(f2(ty.y, 1.f), f2(ty.y, tt.y), gyy_st);
+    g01 = fma2(f2(tx.x, tx.x), f2(tx.x, ty.x), g01);
+    g01 = fma2(f2(tx.y, tx.y), f2(tx.y, ty.y), g01);
+    g2s = fma2(f2(ty.x, 1.f), f2(ty.x, tt.x), g2s);
+    g2s = fma2(f2(ty.y, 1.f), f2(ty.y, tt.y), g2s);
   }
-  gxx_gxy = fma2(f2(t.TXt, t.TXt), f2(t.TXt, t.TYt), gxx_gxy);
-  gyy_st = fma2(f2(t.TYt, 1.f), f2(t.TYt, t.Tt), gyy_st);
-  gxx_gxy = warp_sum2(gxx_gxy);
-  gyy_st = warp_sum2(gyy_st);
-  const double gxx = gxx_gxy.x, gxy = gxx_gxy.y, gyy = gyy_st.x;
+  g01 = warp_sum2(g01);
+  g2s = warp_sum2(g2s);
+  const double gxx = g01.x, gxy = g01.y, gyy = g2s.x;
   const double tr = gxx + gyy;
   const double det = gxx * gyy - gxy * gxy;
   const double lmin =
@@ -307,62 +285,62 @@ __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane&
   const bool finite = isfinite(gxx) && isfinite(gxy) && isfinite(gyy) && isfinite(lmin);
   if (!finite || lmin / N < (double)a.min_eig) {
     if (L > 0) {
-      dx *= 2.0;
-      dy *= 2.0;
+      dx *= 2.0f;
+      dy *= 2.0f;
     } else {
       out.status = V2D_LOST_SMALL_EIG;
     }
     return;
   }
-  // centre the template: T' = T - mean (NCC two-pass; also conditions e = T'-S')
-  const float tmean = gyy_st.y / (float)N;
+  const float i00 = (float)(gyy / det), i01 = (float)(-gxy / det), i11 = (float)(gxx / det);
+  // centre the template: T' = T - mean (two-pass NCC; conditions e = T' - S')
+  const float tmean = g2s.y / (float)N;
   const float valid = lane < WIN ? 1.0f : 0.0f;
-  float2 tt_t1 = f2(0.f, 0.f);  // (sum T'^2, sum T')
+  float2 q = f2(0.f, 0.f);  // (sum T'^2, sum T')
 #pragma unroll
-  for (int p = 0; p < Tmpl<WIN>::NPAIR; ++p) {
-    t.T[p] = __fmul2_rn(sub2(t.T[p], f2(tmean, tmean)), f2(valid, valid));
-    tt_t1 = fma2(f2(t.T[p].x, 1.f), f2(t.T[p].x, t.T[p].x), tt_t1);
-    tt_t1 = fma2(f2(t.T[p].y, 1.f), f2(t.T[p].y, t.T[p].y), tt_t1);
+  for (int p = 0; p < H2; ++p) {
+    const float2 m = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
+    t.T[p] = mul2(sub2(t.T[p], f2(tmean, tmean)), m);
+    q = fma2(f2(t.T[p].x, 1.f), f2(t.T[p].x, t.T[p].x), q);
+    q = fma2(f2(t.T[p].y, 1.f), f2(t.T[p].y, t.T[p].y), q);
   }
-  t.Tt = (t.Tt - tmean) * valid;
-  tt_t1 = fma2(f2(t.Tt, 1.f), f2(t.Tt, t.Tt), tt_t1);
-  const float2 red = warp_sum2(tt_t1);
-  const double Stt0 = red.x, St1 = red.y;
+  q = warp_sum2(q);
+  const double Stt0 = q.x, St1 = q.y;
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
   const int W = J.W, H = J.H;
   int jx0 = 0, jy0 = 0;
   bool staged = false;
-  auto locate = [&](double qx, double qy, int& lc0, int& lr0, float& bx, float& by) {
-    const double fqx = floor(qx), fqy = floor(qy);
+  auto locate = [&](float qx, float qy, int& lc0, int& lr0, float& bx, float& by) {
+    const float fqx = floorf(qx), fqy = floorf(qy);
     const int ixq = (int)fqx, iyq = (int)fqy;
-    bx = (float)(qx - fqx);
-    by = (float)(qy - fqy);
+    bx = qx - fqx;
+    by = qy - fqy;
     lc0 = ixq - R - jx0;
     lr0 = iyq - R - jy0;
     if (!staged || lc0 < 0 || lc0 > 2 * M || lr0 < 0 || lr0 > 2 * M) {
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
-      stage<TJ, SZ>(sp, J, jx0, jy0, tmean);
+      stage(sp, J, jx0, jy0, SZ, tmean);
       staged = true;
       lc0 = M;
       lr0 = M;
     }
   };
+  const float eps2 = a.eps * a.eps;
   for (int it = 1; it <= a.iters; ++it) {
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
     const float2 b = warp_sum2(gn_rhs<WIN>(sp, lc0, lr0, bx, by, t));
-    const double ex = (gyy * (double)b.x - gxy * (double)b.y) / det;
-    const double ey = (gxx * (double)b.y - gxy * (double)b.x) / det;
+    const float ex = fmaf(i00, b.x, i01 * b.y);
+    const float ey = fmaf(i01, b.x, i11 * b.y);
     dx += ex;
     dy += ey;
     out.steps++;
-    const double nx = cx + dx, ny = cy + dy;
-    const bool inside = isfinite(nx) && isfinite(ny) && nx >= 0.0 && nx <= (double)(W - 1) &&
-                        ny >= 0.0 && ny <= (double)(H - 1);
-    if (!inside) {
+    const float nx = cx + dx, ny = cy + dy;
+    const bool inside = nx >= 0.0f && nx <= (float)(W - 1) && ny >= 0.0f && ny <= (float)(H - 1);
+    if (!inside) {  // (also false for NaN)
       if (L > 0) {
         dx -= ex;
         dy -= ey;
@@ -371,7 +349,7 @@ __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane&
       out.status = V2D_LOST_OOB;
       return;
     }
-    if (sqrt(ex * ex + ey * ey) < (double)a.eps) break;
+    if (fmaf(ex, ex, ey * ey) < eps2) break;
   }
   // ---------------- per-level NCC gate --------------------------------------
   {
@@ -380,8 +358,8 @@ __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane&
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
     const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, t);
     const float2 r1 = warp_sum2(f2(mo.x, mo.y));
-    const float2 r2 = warp_sum2(f2(mo.z, 0.f));
-    const double S1 = r1.x, S2 = r1.y, STS = r2.x;
+    const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
+    const double S1 = r1.x, S2 = r1.y, STS = r2;
     const double Stt = Stt0 - St1 * St1 / N;
     const double Sss = S2 - S1 * S1 / N;
     const double Sts = STS - St1 * S1 / N;
@@ -393,24 +371,24 @@ __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane&
     }
   }
   if (L > 0) {
-    dx *= 2.0;
-    dy *= 2.0;
+    dx *= 2.0f;
+    dy *= 2.0f;
   }
 }
 
 template <int WIN>
-__global__ void __launch_bounds__(kThreads, (WIN >= 19 ? 3 : 4))
+__global__ void __launch_bounds__(kThreads, 4)
 klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __restrict__ prev_pyr,
            const uint8_t* const* __restrict__ next_l0, const float* const* __restrict__ next_pyr,
            int B, Levels lv, KltArgs a, const float* __restrict__ pts,
            const float* __restrict__ guess, const uint8_t* __restrict__ in_status,
            float* __restrict__ out_pos, uint8_t* __restrict__ status, float* __restrict__ ncc,
            int32_t* __restrict__ iters_out) {
-  __shared__ float s_patch[kWarps * kPatch];
+  __shared__ float s_mem[kWarps * Smem<WIN>::TOTAL];
   const int64_t warp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (warp >= (int64_t)B * a.P) return;  // warp-uniform
-  float* sp = s_patch + (threadIdx.x >> 5) * kPatch;
+  float* sp = s_mem + (threadIdx.x >> 5) * Smem<WIN>::TOTAL;
   const int b = (int)(warp / a.P);
   const float px = pts[2 * warp], py = pts[2 * warp + 1];
   constexpr int R = (WIN - 1) / 2;
@@ -418,41 +396,41 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
   LevelOut o{V2D_TRACKED, 0.0f, 0, 0};
   const bool skip = (in_status && in_status[warp] != 0) || (px == -1.0f && py == -1.0f) ||
                     !isfinite(px) || !isfinite(py);
-  double dx = 0.0, dy = 0.0;
+  float dx = 0.0f, dy = 0.0f;
   if (skip) {
     o.status = V2D_SKIPPED;
   } else if (px < 0.0f || px > (float)(lv.W[0] - 1) || py < 0.0f || py > (float)(lv.H[0] - 1)) {
     o.status = V2D_LOST_OOB;  // reading #16: a start point outside the image is lost
   } else {
     if (guess) {
-      const double s = 1.0 / (double)(1 << (lv.n - 1));
+      const float s = 1.0f / (float)(1 << (lv.n - 1));
       dx = guess[2 * warp] * s;
       dy = guess[2 * warp + 1] * s;
     }
     for (int L = lv.n - 1; L >= 0 && o.status == V2D_TRACKED; --L) {
-      const double scale = (double)(1 << L);
-      const double cx = ((double)px + 0.5) / scale - 0.5;
-      const double cy = ((double)py + 0.5) / scale - 0.5;
+      const float scale = 1.0f / (float)(1 << L);
+      const float cx = (px + 0.5f) * scale - 0.5f;
+      const float cy = (py + 0.5f) * scale - 0.5f;
+      Plane I, J;
       if (L == 0) {
-        const Plane I{prev_l0[b], a.l0_pitch, lv.W[0], lv.H[0]};
-        const Plane J{next_l0[b], a.l0_pitch, lv.W[0], lv.H[0]};
-        track_level<WIN, uint8_t, uint8_t>(sp, I, J, 0, cx, cy, dx, dy, a, o);
+        I = Plane{prev_l0[b], a.l0_pitch, lv.W[0], lv.H[0], 1};
+        J = Plane{next_l0[b], a.l0_pitch, lv.W[0], lv.H[0], 1};
       } else {
-        const Plane I{prev_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L]};
-        const Plane J{next_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L]};
-        track_level<WIN, float, float>(sp, I, J, L, cx, cy, dx, dy, a, o);
+        I = Plane{prev_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
+        J = Plane{next_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
       }
+      track_level<WIN>(sp, I, J, L, cx, cy, dx, dy, a, o);
     }
   }
   float ox = -1.0f, oy = -1.0f;
   if (o.status == V2D_TRACKED) {
-    const double qx = (double)px + dx, qy = (double)py + dy;
+    const float qx = px + dx, qy = py + dy;
     const int W = lv.W[0], H = lv.H[0];
-    if (qx < R || qx > W - 1 - R || qy < R || qy > H - 1 - R) {
+    if (!(qx >= R && qx <= W - 1 - R && qy >= R && qy <= H - 1 - R)) {
       o.status = V2D_LOST_OOB;
     } else {
-      ox = (float)qx;
-      oy = (float)qy;
+      ox = qx;
+      oy = qy;
     }
   }
   if (lane == 0) {
