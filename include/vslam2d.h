@@ -97,7 +97,7 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
  *   resp       nullable [B][H][W] fp32: full R map (0 outside 2..W-3 x 2..H-3);
  *              when given, the lazy-eigenvalue shortcut is disabled.
  * V2D_EINVAL: border < 3, W or H < 2*border+1, grid cell < 1 px, bad k, nms not
- * 0/1, W*H >= 2^31.  V2D_EALIGN: l0_pitch % 16 != 0. */
+ * 0/1, l0_pitch*H >= 2^31.  V2D_EALIGN: l0_pitch % 16 != 0. */
 int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
                     int grid_x, int grid_y, int k, int K_min, float min_score, int border,
                     int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,

@@ -99,6 +99,7 @@ int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int 
   if (std::isnan(min_score)) return V2D_EINVAL;
   if (grid_k(grid_x, grid_y, k, K_min, &kk)) return V2D_EINVAL;
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
+  if (l0_pitch * (int64_t)H >= ((int64_t)1 << 31)) return V2D_EINVAL;  // 32-bit row offsets
   v2d::GfttArgs a{W, H, grid_x, grid_y, kk, border, nms, min_score, l0_pitch};
   return v2d::launch_gftt(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp,
                           reinterpret_cast<cudaStream_t>(stream));

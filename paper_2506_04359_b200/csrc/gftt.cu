@@ -15,32 +15,35 @@
 //              neighbours' keys (nms = 1)
 //   output   : per cell the k largest candidate keys, descending.
 //
-// B200 mapping: one CTA (256 threads) per (cell, image).  The cell is swept in
-// 32x32 output tiles; each tile stages its u8 footprint (+3 px halo) in shared
-// memory and runs the separable stencil stages there (Sobel -> horizontal
-// 3-sums -> vertical 3-sums + R -> NMS).  Candidates that beat the running
-// per-cell threshold are appended to a shared-memory key buffer which a
-// block-wide bitonic sort periodically folds back to the top k; the threshold
-// then enables the lazy eigenvalue: lambda_min <= min(A',C')/64, so R is only
-// evaluated where that bound can beat the k-th best key (exact — see DESIGN.md
-// §5 K2).  No atomics in global memory, deterministic output.
+// B200 mapping (DESIGN.md §5 K2): one CTA (8 warps) per (cell, image).  The cell
+// is cut into items of 26 output columns x up to 32 rows; a warp owns an item
+// and streams its 32 input columns (3-px halo each side) down the rows with
+// every stage in registers: lane = column, horizontal neighbours by shuffle,
+// vertical windows as rolling registers — no shared-memory staging, no index
+// division.  R rows go to a 3-row per-warp ring in shared memory for the NMS
+// of the (few) lanes that beat the warp's running threshold; those append to a
+// per-warp key buffer that a warp-level bitonic sort folds back to its top k.
+// The threshold also gates the lazy eigenvalue: lambda_min <= min(A',C')/64, so
+// R is only evaluated where that bound can beat the k-th best key (exact: such
+// pixels can neither be selected nor beat a selectable neighbour).  At the end
+// the CTA merges the 8 warps' top-k lists with one block bitonic sort.
+// Deterministic, no global atomics.
 #include "common.cuh"
 
 namespace v2d {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int TS = 32;           // output tile edge
-constexpr int IMG = TS + 6;      // staged u8 edge (halo 3)
-constexpr int IMGP = IMG + 2;    // padded row stride
-constexpr int SOB = TS + 4;      // Sobel edge (halo 2)
-constexpr int RE = TS + 2;       // response edge (halo 1)
-constexpr int kBuf = 2048;       // candidate / top-k key buffer
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kPix = 4;             // adjacent columns per lane (one 32-bit load per row)
+constexpr int kSpan = 32 * kPix;    // columns per warp strip (128)
+constexpr int kOut = kSpan - 8;     // output columns per strip (120): halo 3 left, 5 right
+constexpr int kWBuf = 512;          // per-warp key buffer (top-k + fresh candidates)
+constexpr int kRing = kSpan + 8;    // R ring row (4 pad floats each side)
 
-__device__ __forceinline__ float response_contract(int A, int Bv, int C) {
+__device__ __forceinline__ float response_contract(int A, int Bv, int C, long long det) {
   const int tr = A + C;
   if (tr == 0) return 0.0f;
-  const long long det = (long long)A * C - (long long)Bv * Bv;
   const long long dAC = (long long)(A - C);
   const long long D = dAC * dAC + 4ll * (long long)Bv * Bv;
   const float f_det = __ll2float_rn(det);
@@ -55,17 +58,17 @@ __device__ __forceinline__ unsigned long long make_key(float r, int x, int y, in
   return ((unsigned long long)__float_as_uint(r) << 32) | (unsigned long long)(0xffffffffu - idx);
 }
 
-// Sort buf[0..ntop+ncand) descending and keep the first min(k, total).
-__device__ void fold_topk(unsigned long long* buf, int* s_n, int k) {
-  __syncthreads();
-  const int total = s_n[0] + s_n[1];
+// Descending bitonic sort of buf[0..n), padded with zeros to a power of two, by
+// nthr threads (tid = index within the group); warp or block scope.
+template <bool kBlock>
+__device__ __forceinline__ void bitonic_desc(unsigned long long* buf, int n, int tid, int nthr) {
   int N = 2;
-  while (N < total) N <<= 1;
-  for (int i = total + threadIdx.x; i < N; i += kThreads) buf[i] = 0ull;
-  __syncthreads();
+  while (N < n) N <<= 1;
+  for (int i = n + tid; i < N; i += nthr) buf[i] = 0ull;
+  if (kBlock) __syncthreads(); else __syncwarp();
   for (int size = 2; size <= N; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < (N >> 1); i += kThreads) {
+      for (int i = tid; i < (N >> 1); i += nthr) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool desc = (lo & size) == 0;
@@ -75,32 +78,37 @@ __device__ void fold_topk(unsigned long long* buf, int* s_n, int k) {
           buf[hi] = a;
         }
       }
-      __syncthreads();
+      if (kBlock) __syncthreads(); else __syncwarp();
     }
   }
-  if (threadIdx.x == 0) {
-    s_n[0] = total < k ? total : k;
-    s_n[1] = 0;
-  }
-  __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads)
+// Smallest integer m with (float)m * (2^-6 * (1 + 1e-5)) >= s: pixels whose
+// min(A', C') < m have lambda_min bound below the score s (lazy eigenvalue).
+__device__ __forceinline__ int lazy_int_threshold(float s) {
+  if (!(s > 0.0f)) return 0;
+  const float m = s * (64.0f / 1.00001f);
+  if (m >= 2.0e9f) return 0x7fffffff;
+  return max(0, (int)m - 2);  // conservative by 2 units (fp rounding of the product)
+}
+
+__global__ void __launch_bounds__(kThreads, 6)
 gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
                  float* __restrict__ kp_xy, float* __restrict__ kp_score,
                  int32_t* __restrict__ cell_count, float* __restrict__ resp) {
-  __shared__ uint8_t s_img[IMG * IMGP];
-  __shared__ short2 s_sob[SOB * SOB];
-  __shared__ int s_hA[SOB * RE], s_hB[SOB * RE], s_hC[SOB * RE];
-  __shared__ float s_R[RE * RE];
-  __shared__ unsigned long long s_buf[kBuf];
-  __shared__ int s_n[2];  // [0] = entries kept (top), [1] = appended candidates
+  __shared__ unsigned long long s_buf[kWarps * kWBuf];
+  __shared__ __align__(16) float s_ring[kWarps][3][kRing];
+  __shared__ int s_cnt[kWarps][2];  // [0] = kept (top), [1] = fresh candidates
+  __shared__ int s_total;
+  __shared__ unsigned long long s_thr;  // max over warps of their k-th best key
+  __shared__ int4 s_q[kWarps][kSpan];    // per-warp queue of pixels needing the exact R
 
-  const int W = a.W, H = a.H;
+  const int W = a.W, H = a.H, k = a.k;
   const int cell = blockIdx.x, b = blockIdx.y;
   const int cx = cell % a.grid_x, cy = cell / a.grid_x;
   const uint8_t* __restrict__ img = l0_ptrs[b];
   const int64_t pitch = a.pitch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // D6 cell: [floor(cx*W/gx), floor((cx+1)*W/gx)) x [...]
   const int x0 = (int)((int64_t)cx * W / a.grid_x), x1 = (int)((int64_t)(cx + 1) * W / a.grid_x);
@@ -111,129 +119,248 @@ gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
   const int rx0 = full ? x0 : max(x0, ex0), rx1 = full ? x1 : min(x1, ex1);
   const int ry0 = full ? y0 : max(y0, ey0), ry1 = full ? y1 : min(y1, ey1);
   const bool lazy = !full;
-  const int max_per_tile = a.nms ? (TS * TS) / 4 : TS * TS;
-  const int early = max(64, 2 * a.k);
 
-  if (threadIdx.x == 0) {
-    s_n[0] = 0;
-    s_n[1] = 0;
+  unsigned long long* wbuf = s_buf + warp * kWBuf;
+  float (*ring)[kRing] = s_ring[warp];
+  if (lane == 0) {
+    s_cnt[warp][0] = 0;
+    s_cnt[warp][1] = 0;
   }
+  if (threadIdx.x == 0) s_thr = 0ull;
+  for (int i = lane; i < 3 * kRing; i += 32) (&ring[0][0])[i] = 0.0f;
   __syncthreads();
 
-  for (int ty = ry0; ty < ry1; ty += TS) {
-    for (int tx = rx0; tx < rx1; tx += TS) {
-      // running threshold (score part used by the lazy eigenvalue bound)
-      const int ntop = s_n[0];
-      const unsigned long long thr = (ntop == a.k) ? s_buf[a.k - 1] : 0ull;
-      const float thr_score = __uint_as_float((unsigned)(thr >> 32));
+  // strips of kOut output columns starting 4-aligned (xs = first loaded column)
+  const int xs0 = ((rx0 - 3) >> 2) << 2;  // floor to a multiple of 4
+  const int nxs = rx1 > rx0 ? (rx1 - (xs0 + 3) + kOut - 1) / kOut : 0;
+  // row chunks: aim for >= kWarps items per cell, >= 8 rows per chunk
+  const int rows = ry1 - ry0;
+  int nys = rows > 0 ? max(1, (kWarps + nxs - 1) / max(nxs, 1)) : 0;
+  nys = min(nys, max(1, rows / 8));
+  const int chunk = nys > 0 ? (rows + nys - 1) / nys : 0;
+  const int items = nxs * nys;
+  const int fold_at = max(64, 2 * k);
 
-      // ---- stage u8 footprint (clamped reads; out-of-image values are
-      //      never used by an in-domain response) -------------------------
-      for (int i = threadIdx.x; i < IMG * IMG; i += kThreads) {
-        const int jj = i / IMG, ii = i % IMG;
-        const int gx = min(max(tx - 3 + ii, 0), W - 1);
-        const int gy = min(max(ty - 3 + jj, 0), H - 1);
-        s_img[jj * IMGP + ii] = __ldg(img + (int64_t)gy * pitch + gx);
-      }
-      __syncthreads();
-      // ---- integer Sobel (sx = 8 Gx, sy = 8 Gy) --------------------------
-      for (int i = threadIdx.x; i < SOB * SOB; i += kThreads) {
-        const int jj = i / SOB, ii = i % SOB;
-        const uint8_t* r0 = s_img + jj * IMGP + ii;
-        const uint8_t* r1 = r0 + IMGP;
-        const uint8_t* r2 = r1 + IMGP;
-        const int sx = (r0[2] + 2 * r1[2] + r2[2]) - (r0[0] + 2 * r1[0] + r2[0]);
-        const int sy = (r2[0] + 2 * r2[1] + r2[2]) - (r0[0] + 2 * r0[1] + r0[2]);
-        s_sob[i] = make_short2((short)sx, (short)sy);
-      }
-      __syncthreads();
-      // ---- horizontal 3-sums of the tensor products ----------------------
-      for (int i = threadIdx.x; i < SOB * RE; i += kThreads) {
-        const int jj = i / RE, ii = i % RE;
-        const short2* s = s_sob + jj * SOB + ii;
-        int A = 0, Bv = 0, C = 0;
+  for (int item = warp; item < items; item += kWarps) {
+    const int sy_ = item / nxs, sx_ = item - sy_ * nxs;
+    const int xs = xs0 + sx_ * kOut;
+    const int oy = ry0 + sy_ * chunk;
+    const int oy_end = min(oy + chunk, ry1);
+    const int xl = xs + kPix * lane;      // this lane's first column
+    const bool load_ok = xl >= 0 && xl < pitch;  // 4-aligned word inside the row
+    const uint8_t* __restrict__ colp = img + (load_ok ? xl : 0);
+    const int ipitch = (int)pitch;  // W*H < 2^31 is validated by the ABI
+
+    int i0[kPix] = {0, 0, 0, 0}, i1[kPix] = {0, 0, 0, 0};  // I rows L-2, L-1
+    int hs0[kPix] = {0, 0, 0, 0}, hs1[kPix] = {0, 0, 0, 0};  // [1 2 1]_x rows L-2, L-1
+    int a0[kPix] = {0, 0, 0, 0}, a1[kPix] = {0, 0, 0, 0};
+    int b0[kPix] = {0, 0, 0, 0}, b1[kPix] = {0, 0, 0, 0};
+    int c0[kPix] = {0, 0, 0, 0}, c1[kPix] = {0, 0, 0, 0};
+    int ridx = 0;
+    auto ld_row = [&](int L) -> unsigned {
+      const int yc = min(max(L, 0), H - 1);
+      return load_ok ? __ldg(reinterpret_cast<const unsigned*>(colp + (unsigned)(yc * ipitch))) : 0u;
+    };
+    // software pipeline: rows L+1 and L+2 are in flight while row L is processed
+    unsigned w_n1 = ld_row(oy - 3), w_n2 = ld_row(oy - 2);
+    for (int L = oy - 3; L <= oy_end + 2; ++L) {
+      const unsigned w = w_n1;
+      w_n1 = w_n2;
+      w_n2 = ld_row(L + 2);
+      const unsigned wl = __shfl_up_sync(kFullMask, w, 1);
+      const unsigned wr = __shfl_down_sync(kFullMask, w, 1);
+      int I[kPix + 2];
+      I[0] = (int)(wl >> 24);
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const int gx = s[d].x, gy = s[d].y;
-          A += gx * gx;
-          Bv += gx * gy;
-          C += gy * gy;
-        }
-        s_hA[i] = A;
-        s_hB[i] = Bv;
-        s_hC[i] = C;
+      for (int j = 0; j < kPix; ++j) I[j + 1] = (int)((w >> (8 * j)) & 0xffu);
+      I[kPix + 1] = (int)(wr & 0xffu);
+      int hs[kPix], V[kPix + 2];
+#pragma unroll
+      for (int j = 0; j < kPix; ++j) {
+        hs[j] = I[j] + 2 * I[j + 1] + I[j + 2];
+        V[j + 1] = i0[j] + 2 * i1[j] + I[j + 1];
       }
-      __syncthreads();
-      // ---- vertical 3-sums + response (lazy) -----------------------------
-      for (int i = threadIdx.x; i < RE * RE; i += kThreads) {
-        const int jj = i / RE, ii = i % RE;
-        const int px = tx - 1 + ii, py = ty - 1 + jj;
-        float r = 0.0f;
-        if (px >= 2 && px <= W - 3 && py >= 2 && py <= H - 3) {
-          const int o = jj * RE + ii;
-          const int A = s_hA[o] + s_hA[o + RE] + s_hA[o + 2 * RE];
-          const int C = s_hC[o] + s_hC[o + RE] + s_hC[o + 2 * RE];
-          // lambda_min <= min(A',C')/64; the 1e-5 slack covers fp32 rounding
-          // of the contract value (<= ~5 ulp).
-          const float ub = (float)min(A, C) * (0.015625f * 1.00001f);
-          if (!lazy || ub >= thr_score) {
-            const int Bv = s_hB[o] + s_hB[o + RE] + s_hB[o + 2 * RE];
-            r = response_contract(A, Bv, C);
+      V[0] = __shfl_up_sync(kFullMask, V[kPix], 1);
+      V[kPix + 1] = __shfl_down_sync(kFullMask, V[1], 1);
+      // Sobel at row L-1 and tensor products
+      int pa[kPix + 2], pb[kPix + 2], pc[kPix + 2];
+#pragma unroll
+      for (int j = 0; j < kPix; ++j) {
+        const int sx = V[j + 2] - V[j];
+        const int sy = hs[j] - hs0[j];
+        pa[j + 1] = sx * sx;
+        pb[j + 1] = sx * sy;
+        pc[j + 1] = sy * sy;
+      }
+      pa[0] = __shfl_up_sync(kFullMask, pa[kPix], 1);
+      pb[0] = __shfl_up_sync(kFullMask, pb[kPix], 1);
+      pc[0] = __shfl_up_sync(kFullMask, pc[kPix], 1);
+      pa[kPix + 1] = __shfl_down_sync(kFullMask, pa[1], 1);
+      pb[kPix + 1] = __shfl_down_sync(kFullMask, pb[1], 1);
+      pc[kPix + 1] = __shfl_down_sync(kFullMask, pc[1], 1);
+      // running threshold: any warp's k-th best key bounds the cell's k-th key
+      // from below, so the largest one is a valid pruning threshold for all
+      const int ntop = s_cnt[warp][0];
+      const unsigned long long thr =
+          lazy ? max(ntop == k ? wbuf[k - 1] : 0ull, *(volatile unsigned long long*)&s_thr) : 0ull;
+      const float thr_score = __uint_as_float((unsigned)(thr >> 32));
+      const int lz = lazy ? lazy_int_threshold(thr_score) : 0;
+      const int yr = L - 2;  // tensor / response row
+      const bool yr_ok = yr >= 2 && yr <= H - 3;
+      int ha[kPix], hb[kPix], hc[kPix];
+      int need_pos[kPix];
+      int nq = 0;
+      const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+      for (int j = 0; j < kPix; ++j) {
+        ha[j] = pa[j] + pa[j + 1] + pa[j + 2];
+        hb[j] = pb[j] + pb[j + 1] + pb[j + 2];
+        hc[j] = pc[j] + pc[j + 1] + pc[j + 2];
+        const int A = a0[j] + a1[j] + ha[j];
+        const int C = c0[j] + c1[j] + hc[j];
+        const int Bv = b0[j] + b1[j] + hb[j];
+        const int x = xl + j;
+        bool need = yr_ok && x >= 2 && x <= W - 3 && min(A, C) >= lz;
+        if (need && lazy) {
+          // tighter exact bound lambda_min <= 2 det / tr (lambda_max >= tr/2)
+          const long long det = (long long)A * C - (long long)Bv * Bv;
+          need = __ll2float_rn(det) * (2.0f / 64.0f) >= thr_score * 0.99999f * __int2float_rn(A + C);
+        }
+        const unsigned msk = __ballot_sync(kFullMask, need);
+        need_pos[j] = need ? nq + __popc(msk & lt_mask) : -1;
+        nq += __popc(msk);
+        if (need) s_q[warp][need_pos[j]] = make_int4(A, Bv, C, 4 + kPix * lane + j);
+      }
+      ridx = ridx == 2 ? 0 : ridx + 1;
+      *reinterpret_cast<float4*>(&ring[ridx][4 + kPix * lane]) = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+      // exact fp32-contract response for the queued pixels, 32 at a time
+      for (int q = lane; q < nq; q += 32) {
+        const int4 e = s_q[warp][q];
+        const long long det = (long long)e.x * e.z - (long long)e.y * e.y;
+        ring[ridx][e.w] = response_contract(e.x, e.y, e.z, det);
+      }
+      __syncwarp();
+      if (full && yr >= oy && yr < oy_end) {
+#pragma unroll
+        for (int j = 0; j < kPix; ++j) {
+          const int x = xl + j;
+          if (x >= xs + 3 && x < xs + 3 + kOut && x >= rx0 && x < rx1)
+            resp[((int64_t)b * H + yr) * W + x] = ring[ridx][4 + kPix * lane + j];
+        }
+      }
+      // NMS + threshold at row yn = L-3 (ring rows: ru = yn-1, rm = yn, rd = yn+1).
+      // With R >= 0 the key order is: p beats the 4 neighbours BEFORE it in
+      // row-major order iff R(p) > R(q), the 4 AFTER it iff R(p) >= R(q).
+      const int yn = L - 3;
+      if (yn >= oy && yn < oy_end && yn >= ey0 && yn < ey1) {
+        const int rm = ridx == 0 ? 2 : ridx - 1;
+        const int ru = rm == 0 ? 2 : rm - 1;
+        float u[kPix + 2], m[kPix + 2], d[kPix + 2];
+        {
+          const int c = 4 + kPix * lane;
+          const float4 u4 = *reinterpret_cast<const float4*>(&ring[ru][c]);
+          const float4 m4 = *reinterpret_cast<const float4*>(&ring[rm][c]);
+          const float4 d4 = *reinterpret_cast<const float4*>(&ring[ridx][c]);
+          u[0] = ring[ru][c - 1]; m[0] = ring[rm][c - 1]; d[0] = ring[ridx][c - 1];
+          u[1] = u4.x; u[2] = u4.y; u[3] = u4.z; u[4] = u4.w;
+          m[1] = m4.x; m[2] = m4.y; m[3] = m4.z; m[4] = m4.w;
+          d[1] = d4.x; d[2] = d4.y; d[3] = d4.z; d[4] = d4.w;
+          u[5] = ring[ru][c + 4]; m[5] = ring[rm][c + 4]; d[5] = ring[ridx][c + 4];
+        }
+#pragma unroll
+        for (int j = 0; j < kPix; ++j) {
+          const float rp = m[j + 1];
+          const int x = xl + j;
+          bool ok = rp > a.min_score && rp >= thr_score && x >= xs + 3 && x < xs + 3 + kOut &&
+                    x >= rx0 && x < rx1 && x >= ex0 && x < ex1;
+          if (a.nms)
+            ok = ok && rp > u[j] && rp > u[j + 1] && rp > u[j + 2] && rp > m[j] &&
+                 rp >= m[j + 2] && rp >= d[j] && rp >= d[j + 1] && rp >= d[j + 2];
+          if (ok) {
+            const unsigned long long kp = make_key(rp, x, yn, W);
+            if (kp > thr) {
+              const int slot = atomicAdd(&s_cnt[warp][1], 1);
+              wbuf[ntop + slot] = kp;
+            }
           }
         }
-        s_R[i] = r;
-        if (full && ii >= 1 && ii <= TS && jj >= 1 && jj <= TS && px < x1 && py < y1)
-          resp[((int64_t)b * H + py) * W + px] = r;
       }
-      __syncthreads();
-      // ---- eligibility + NMS + threshold -> append -----------------------
-      for (int i = threadIdx.x; i < TS * TS; i += kThreads) {
-        const int jj = i / TS, ii = i % TS;
-        const int px = tx + ii, py = ty + jj;
-        if (px >= rx1 || py >= ry1) continue;
-        if (px < ex0 || px >= ex1 || py < ey0 || py >= ey1) continue;
-        const int o = (jj + 1) * RE + (ii + 1);
-        const float r = s_R[o];
-        if (!(r > a.min_score)) continue;
-        const unsigned long long kp = make_key(r, px, py, W);
-        if (kp <= thr) continue;
-        bool ok = true;
-        if (a.nms) {
-#pragma unroll
-          for (int dj = -1; dj <= 1; ++dj)
-#pragma unroll
-            for (int di = -1; di <= 1; ++di) {
-              if (di == 0 && dj == 0) continue;
-              const unsigned long long kq = make_key(s_R[o + dj * RE + di], px + di, py + dj, W);
-              ok = ok && (kp > kq);
-            }
+      __syncwarp();
+      const int nc = s_cnt[warp][1];
+      if (nc > 0 && (ntop + nc + kSpan > kWBuf || (lazy && nc >= fold_at))) {
+        bitonic_desc<false>(wbuf, ntop + nc, lane, 32);
+        if (lane == 0) {
+          s_cnt[warp][0] = min(ntop + nc, k);
+          s_cnt[warp][1] = 0;
+          if (ntop + nc >= k) atomicMax(&s_thr, wbuf[k - 1]);
         }
-        if (ok) {
-          const int slot = atomicAdd(&s_n[1], 1);
-          s_buf[ntop + slot] = kp;
-        }
+        __syncwarp();
       }
-      __syncthreads();
-      const int nc = s_n[1];
-      if (s_n[0] + nc + max_per_tile > kBuf || (lazy && nc >= early)) fold_topk(s_buf, s_n, a.k);
+#pragma unroll
+      for (int j = 0; j < kPix; ++j) {
+        i0[j] = i1[j]; i1[j] = I[j + 1];
+        hs0[j] = hs1[j]; hs1[j] = hs[j];
+        a0[j] = a1[j]; a1[j] = ha[j];
+        b0[j] = b1[j]; b1[j] = hb[j];
+        c0[j] = c1[j]; c1[j] = hc[j];
+      }
     }
   }
-  if (s_n[1] > 0) fold_topk(s_buf, s_n, a.k);
+  // fold each warp's remaining candidates
+  {
+    const int ntop = s_cnt[warp][0], nc = s_cnt[warp][1];
+    if (nc > 0) {
+      bitonic_desc<false>(wbuf, ntop + nc, lane, 32);
+      if (lane == 0) {
+        s_cnt[warp][0] = min(ntop + nc, k);
+        s_cnt[warp][1] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- CTA merge of the warps' top-k lists --------------------------------
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      s_cnt[w][1] = off;  // reuse as prefix offset
+      off += s_cnt[w][0];
+    }
+    s_total = off;
+  }
+  __syncthreads();
+  unsigned long long tmp[V2D_MAX_K / 32];
+  const int nmine = s_cnt[warp][0], dst = s_cnt[warp][1];
+#pragma unroll
+  for (int j = 0; j < V2D_MAX_K / 32; ++j) {
+    const int i = lane + 32 * j;
+    tmp[j] = i < nmine ? wbuf[i] : 0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < V2D_MAX_K / 32; ++j) {
+    const int i = lane + 32 * j;
+    if (i < nmine) s_buf[dst + i] = tmp[j];
+  }
+  __syncthreads();
+  const int total = s_total;
+  if (total > 1) bitonic_desc<true>(s_buf, total, threadIdx.x, kThreads);
+  __syncthreads();
+  const int ntop = min(total, k);
 
-  // ---- emit the cell's slots (D6 slot order) -----------------------------
-  const int ntop = s_n[0];
-  const int64_t base = ((int64_t)(b * a.grid_y + cy) * a.grid_x + cx) * a.k;
-  for (int s = threadIdx.x; s < a.k; s += kThreads) {
-    float x = -1.0f, y = -1.0f, sc = 0.0f;
+  // ---- emit the cell's slots (D6 slot order) -------------------------------
+  const int64_t base = ((int64_t)(b * a.grid_y + cy) * a.grid_x + cx) * k;
+  for (int s = threadIdx.x; s < k; s += kThreads) {
+    float xo = -1.0f, yo = -1.0f, sc = 0.0f;
     if (s < ntop) {
       const unsigned long long kk = s_buf[s];
       const unsigned idx = 0xffffffffu - (unsigned)(kk & 0xffffffffull);
-      x = (float)(idx % (unsigned)W);
-      y = (float)(idx / (unsigned)W);
+      xo = (float)(idx % (unsigned)W);
+      yo = (float)(idx / (unsigned)W);
       sc = __uint_as_float((unsigned)(kk >> 32));
     }
-    kp_xy[2 * (base + s)] = x;
-    kp_xy[2 * (base + s) + 1] = y;
+    kp_xy[2 * (base + s)] = xo;
+    kp_xy[2 * (base + s) + 1] = yo;
     kp_score[base + s] = sc;
   }
   if (threadIdx.x == 0) cell_count[(int64_t)b * a.grid_x * a.grid_y + cell] = ntop;
