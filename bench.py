@@ -42,8 +42,8 @@ DEFAULT_CONFIG = "c2"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(synth.WORKLOADS))
     ap.add_argument("--frames-per-step", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -110,7 +110,7 @@ class Clocks:
         if shutil.which("nvidia-smi"):
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
 
     def stop(self):
@@ -415,6 +415,8 @@ def main():
         "kernels": {n: {"ms_per_launch": float(k_ms[j]), "share_of_step": float(k_ms[j] / (ms / args.steps))}
                     for j, n in enumerate(names)},
         "gpu_launches": 3 * args.steps,
+        "klt_work": {"gn_steps_per_attempted_kp": float((iters_np & 0xFFFFFF).sum()) / max(attempted, 1),
+                     "levels_per_attempted_kp": float((iters_np >> 24).sum()) / max(attempted, 1)},
         "peaks": pk,
         "clocks": clock_rec,
     }

@@ -92,7 +92,7 @@ __device__ __forceinline__ int lazy_int_threshold(float s) {
   return max(0, (int)m - 2);  // conservative by 2 units (fp rounding of the product)
 }
 
-__global__ void __launch_bounds__(kThreads, 6)
+__global__ void __launch_bounds__(kThreads)
 gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
                  float* __restrict__ kp_xy, float* __restrict__ kp_score,
                  int32_t* __restrict__ cell_count, float* __restrict__ resp) {

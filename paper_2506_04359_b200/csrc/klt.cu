@@ -70,29 +70,45 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
   return v;
 }
 
-// Stage rows [oy, oy+nrows) x columns [ox, ox+32) of a level (clamp-to-edge)
-// into a warp patch, minus `shift` (lane = column).
-__device__ __forceinline__ void stage(float* __restrict__ sp, const Plane& pl, int ox, int oy,
-                                      int nrows, float shift) {
+// Stage rows [oy, oy+nr) x columns [ox, ox+32) of a level (clamp-to-edge)
+// into a warp patch, minus `shift` (lane = column).  Out of line and only
+// lightly unrolled: the kernel is instruction-cache bound, staging is not.
+template <typename T>
+__device__ __noinline__ void stage_t(float* __restrict__ sp, const T* __restrict__ base,
+                                     int64_t pitch, int W, int H, int ox, int oy, int nr,
+                                     float shift) {
   const int lane = threadIdx.x & 31;
-  const int x = clampi(ox + lane, 0, pl.W - 1);
+  const T* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
-  if (pl.u8) {
-    const uint8_t* __restrict__ col = reinterpret_cast<const uint8_t*>(pl.base) + x;
-#pragma unroll 4
-    for (int r = 0; r < nrows; ++r) {
-      const int y = clampi(oy + r, 0, pl.H - 1);
-      sp[r * kPitch + lane] = (float)__ldg(col + (int64_t)y * pl.pitch) - shift;
+  if (oy >= 0 && oy + nr <= H) {
+    const T* __restrict__ p = col + (int64_t)oy * pitch;
+    int r = 0;
+    for (; r + 4 <= nr; r += 4, p += 4 * pitch) {
+      const float v0 = (float)__ldg(p), v1 = (float)__ldg(p + pitch);
+      const float v2 = (float)__ldg(p + 2 * pitch), v3 = (float)__ldg(p + 3 * pitch);
+      sp[r * kPitch + lane] = v0 - shift;
+      sp[(r + 1) * kPitch + lane] = v1 - shift;
+      sp[(r + 2) * kPitch + lane] = v2 - shift;
+      sp[(r + 3) * kPitch + lane] = v3 - shift;
     }
+    for (; r < nr; ++r, p += pitch) sp[r * kPitch + lane] = (float)__ldg(p) - shift;
   } else {
-    const float* __restrict__ col = reinterpret_cast<const float*>(pl.base) + x;
-#pragma unroll 4
-    for (int r = 0; r < nrows; ++r) {
-      const int y = clampi(oy + r, 0, pl.H - 1);
-      sp[r * kPitch + lane] = __ldg(col + (int64_t)y * pl.pitch) - shift;
+    for (int r = 0; r < nr; ++r) {
+      const int y = clampi(oy + r, 0, H - 1);
+      sp[r * kPitch + lane] = (float)__ldg(col + (int64_t)y * pitch) - shift;
     }
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ void stage(float* __restrict__ sp, const Plane& pl, int ox, int oy,
+                                      int nr, float shift) {
+  if (pl.u8)
+    stage_t<uint8_t>(sp, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy,
+                     nr, shift);
+  else
+    stage_t<float>(sp, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr,
+                   shift);
 }
 
 struct LevelOut {
@@ -124,20 +140,50 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
   const int lane = threadIdx.x & 31;
   const int c = min(lane, WIN);
   if ((ix - R >= 0) && (ix + R + 1 <= W - 1) && (iy - R >= 0) && (iy + R + 1 <= H - 1)) {
-    // every grid centre inside the image: rolling 3x3 Sobel over patch rows
-    float l0 = P[c], m0 = P[c + 1], r0 = P[c + 2];
-    float l1 = P[kPitch + c], m1 = P[kPitch + c + 1], r1 = P[kPitch + c + 2];
-#pragma unroll 2
-    for (int g = 0; g <= WIN; ++g) {
-      const float* row = P + (g + 2) * kPitch;
-      const float l2 = row[c], m2 = row[c + 1], r2 = row[c + 2];
-      GX[g * kPitch + lane] = ((r0 + 2.f * r1 + r2) - (l0 + 2.f * l1 + l2)) * 0.125f;
-      GY[g * kPitch + lane] = ((l2 + 2.f * m2 + r2) - (l0 + 2.f * m0 + r0)) * 0.125f;
-      l0 = l1; m0 = m1; r0 = r1;
-      l1 = l2; m1 = m2; r1 = r2;
+    // Every grid centre is inside the image, so bilinear(Sobel/8) is the
+    // separable 4x4 filter: with patch columns P0..P3 = P[.][u..u+3],
+    //   Dx = (1-ax)(P2-P0) + ax(P3-P1)          Hs = (1-ax)S(u+1) + ax S(u+2)
+    //   Tx(v) = [(1-ay)V(v) + ay V(v+1)]/8,     V(v) = Dx(v) + 2Dx(v+1) + Dx(v+2)
+    //   Ty(v) = [(1-ay)E(v) + ay E(v+1)]/8,     E(v) = Hs(v+2) - Hs(v)
+    //   T(v)  = (1-ay)h(v+1) + ay h(v+2),       h = (1-ax)P1 + ax P2
+    // over patch rows (v = patch row - 3); rows in split pairs (q, q+H2-1).
+    const int u = min(lane, WIN - 1);
+    const float2 wx = f2(ax, ax), wy = f2(ay, ay), two = f2(2.f, 2.f);
+    const float2 eighth = f2(0.125f, 0.125f);
+    float2 dx0 = f2(0.f, 0.f), dx1 = dx0, dx2 = dx0;   // Dx rows q-3..q-1
+    float2 hs0 = dx0, hs1 = dx0, hs2 = dx0;            // Hs rows q-3..q-1
+    float2 h1 = dx0, h2 = dx0;                         // h rows q-2, q-1
+    float2 vprev = dx0, eprev = dx0;
+#pragma unroll
+    for (int q = 0; q < H2 + 3; ++q) {
+      const float* ra = P + q * kPitch + u;
+      const float* rb = P + (q + H2 - 1) * kPitch + u;
+      const float2 p0 = f2(ra[0], rb[0]), p1 = f2(ra[1], rb[1]);
+      const float2 p2 = f2(ra[2], rb[2]), p3 = f2(ra[3], rb[3]);
+      const float2 d0 = sub2(p2, p0), d1 = sub2(p3, p1);
+      const float2 dx = fma2(wx, sub2(d1, d0), d0);
+      const float2 s0 = fma2(two, p1, add2(p0, p2)), s1 = fma2(two, p2, add2(p1, p3));
+      const float2 hs = fma2(wx, sub2(s1, s0), s0);
+      const float2 h = fma2(wx, sub2(p2, p1), p1);
+      // V(q-2) = Dx(q-2) + 2Dx(q-1) + Dx(q),  E(q-2) = Hs(q) - Hs(q-2)
+      const float2 vq = fma2(two, dx2, add2(dx1, dx));
+      const float2 eq = sub2(hs, hs1);
+      if (q >= 3) {
+        const int pq = q - 3;  // output pair index (rows v = q-3 and q-3+H2-1)
+        t.T[pq] = fma2(wy, sub2(h2, h1), h1);
+        t.TX[pq] = mul2(fma2(wy, sub2(vq, vprev), vprev), eighth);
+        t.TY[pq] = mul2(fma2(wy, sub2(eq, eprev), eprev), eighth);
+      }
+      vprev = vq;
+      eprev = eq;
+      dx0 = dx1; dx1 = dx2; dx2 = dx;
+      hs0 = hs1; hs1 = hs2; hs2 = hs;
+      h1 = h2; h2 = h;
     }
   } else {
-    // near a border: gradient at the clamped centre
+    // near a border: the gradient image is clamped, so build the clamped
+    // gradient grids (grid point (c, g) <-> pixel (ix-R+c, iy-R+g), sampled at
+    // the clamped centre) and interpolate them
     const int lc = clampi(ix - R + c, 0, W - 1) - (ix - R - 1);
     for (int g = 0; g <= WIN; ++g) {
       const int lr = clampi(iy - R + g, 0, H - 1) - (iy - R - 1);
@@ -149,31 +195,31 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       GY[g * kPitch + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
                                (up[lc - 1] + 2.f * up[lc] + up[lc + 1])) * 0.125f;
     }
-  }
-  __syncwarp();
-  // bilinear samples (shared weights ax, ay): T row v from patch rows v+1, v+2 /
-  // cols u+1, u+2; Tx, Ty row v from grid rows v, v+1 / cols u, u+1.
-  const int u = min(lane, WIN - 1);
-  const float2 wx = f2(ax, ax), wy = f2(ay, ay);
-  auto hrow = [&](const float* base, int ra, int rb, int col) {
-    const float2 a0 = f2(base[ra * kPitch + col], base[rb * kPitch + col]);
-    const float2 a1 = f2(base[ra * kPitch + col + 1], base[rb * kPitch + col + 1]);
-    return fma2(wx, sub2(a1, a0), a0);
-  };
-  float2 hp = hrow(P, 1, H2, u + 1);
-  float2 hx = hrow(GX, 0, H2 - 1, u);
-  float2 hy = hrow(GY, 0, H2 - 1, u);
+    __syncwarp();
+    // T row v from patch rows v+1, v+2 / cols u+1, u+2; Tx, Ty row v from grid
+    // rows v, v+1 / cols u, u+1 (shared bilinear weights)
+    const int u = min(lane, WIN - 1);
+    const float2 wx = f2(ax, ax), wy = f2(ay, ay);
+    auto hrow = [&](const float* base, int ra, int rb, int col) {
+      const float2 a0 = f2(base[ra * kPitch + col], base[rb * kPitch + col]);
+      const float2 a1 = f2(base[ra * kPitch + col + 1], base[rb * kPitch + col + 1]);
+      return fma2(wx, sub2(a1, a0), a0);
+    };
+    float2 hp = hrow(P, 1, H2, u + 1);
+    float2 hx = hrow(GX, 0, H2 - 1, u);
+    float2 hy = hrow(GY, 0, H2 - 1, u);
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
-    const float2 np = hrow(P, p + 2, p + H2 + 1, u + 1);
-    const float2 nx = hrow(GX, p + 1, p + H2, u);
-    const float2 ny = hrow(GY, p + 1, p + H2, u);
-    t.T[p] = fma2(wy, sub2(np, hp), hp);
-    t.TX[p] = fma2(wy, sub2(nx, hx), hx);
-    t.TY[p] = fma2(wy, sub2(ny, hy), hy);
-    hp = np;
-    hx = nx;
-    hy = ny;
+    for (int p = 0; p < H2; ++p) {
+      const float2 np = hrow(P, p + 2, p + H2 + 1, u + 1);
+      const float2 nx = hrow(GX, p + 1, p + H2, u);
+      const float2 ny = hrow(GY, p + 1, p + H2, u);
+      t.T[p] = fma2(wy, sub2(np, hp), hp);
+      t.TX[p] = fma2(wy, sub2(nx, hx), hx);
+      t.TY[p] = fma2(wy, sub2(ny, hy), hy);
+      hp = np;
+      hx = nx;
+      hy = ny;
+    }
   }
   const float valid = lane < WIN ? 1.0f : 0.0f;
   const float2 vv = f2(valid, valid);
@@ -277,13 +323,13 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   }
   g01 = warp_sum2(g01);
   g2s = warp_sum2(g2s);
-  const double gxx = g01.x, gxy = g01.y, gyy = g2s.x;
-  const double tr = gxx + gyy;
-  const double det = gxx * gyy - gxy * gxy;
-  const double lmin =
-      tr == 0.0 ? 0.0 : det / (0.5 * (tr + sqrt((gxx - gyy) * (gxx - gyy) + 4.0 * gxy * gxy)));
-  const bool finite = isfinite(gxx) && isfinite(gxy) && isfinite(gyy) && isfinite(lmin);
-  if (!finite || lmin / N < (double)a.min_eig) {
+  // lambda_min(G)/n < min_eig  <=>  det < min_eig * n * lambda_max  (no division)
+  const float gxx = g01.x, gxy = g01.y, gyy = g2s.x;
+  const float det = (float)((double)gxx * gyy - (double)gxy * gxy);  // no cancellation
+  const float dg = gxx - gyy;
+  const float lmax = 0.5f * (gxx + gyy + sqrtf(fmaf(dg, dg, 4.0f * gxy * gxy)));
+  const bool finite = isfinite(gxx) && isfinite(gxy) && isfinite(gyy) && isfinite(det);
+  if (!finite || !(det > 0.0f) || det < a.min_eig * (float)N * lmax) {
     if (L > 0) {
       dx *= 2.0f;
       dy *= 2.0f;
@@ -292,7 +338,8 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     }
     return;
   }
-  const float i00 = (float)(gyy / det), i01 = (float)(-gxy / det), i11 = (float)(gxx / det);
+  const float inv_det = 1.0f / det;
+  const float i00 = gyy * inv_det, i01 = -gxy * inv_det, i11 = gxx * inv_det;
   // centre the template: T' = T - mean (two-pass NCC; conditions e = T' - S')
   const float tmean = g2s.y / (float)N;
   const float valid = lane < WIN ? 1.0f : 0.0f;
@@ -305,7 +352,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     q = fma2(f2(t.T[p].y, 1.f), f2(t.T[p].y, t.T[p].y), q);
   }
   q = warp_sum2(q);
-  const double Stt0 = q.x, St1 = q.y;
+  const float Stt = q.x - q.y * q.y * (1.0f / (float)N);  // sum (T - mean)^2
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
   const int W = J.W, H = J.H;
@@ -359,12 +406,13 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, t);
     const float2 r1 = warp_sum2(f2(mo.x, mo.y));
     const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
-    const double S1 = r1.x, S2 = r1.y, STS = r2;
-    const double Stt = Stt0 - St1 * St1 / N;
-    const double Sss = S2 - S1 * S1 / N;
-    const double Sts = STS - St1 * S1 / N;
-    const double den = sqrt(Stt * Sss);
-    out.ncc = den > 0.0 ? (float)(Sts / den) : 0.0f;
+    // two-pass NCC: T' = T - mean is centred; S' = S - mean_T, so
+    // sum(S-Sm)^2 = sum S'^2 - (sum S')^2/n and sum(T-Tm)(S-Sm) = sum T'S'
+    // - (sum T')(sum S')/n with sum T' ~ 0
+    const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
+    const float Sts = r2 - q.y * r1.x * (1.0f / (float)N);
+    const float den2 = Stt * Sss;
+    out.ncc = den2 > 0.0f ? Sts * rsqrtf(den2) : 0.0f;
     if (out.ncc < a.ncc_min) {
       out.status = V2D_LOST_NCC;
       return;
@@ -408,7 +456,7 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
       dy = guess[2 * warp + 1] * s;
     }
     for (int L = lv.n - 1; L >= 0 && o.status == V2D_TRACKED; --L) {
-      const float scale = 1.0f / (float)(1 << L);
+      const float scale = __int_as_float((127 - L) << 23);  // 2^-L exactly
       const float cx = (px + 0.5f) * scale - 0.5f;
       const float cy = (py + 0.5f) * scale - 0.5f;
       Plane I, J;
