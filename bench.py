@@ -259,6 +259,7 @@ def main():
 
     from paper_2506_04359_b200 import vslam2d as v2d
     from paper_2506_04359_b200.frontend import Frontend2D, RingSchedule
+    from paper_2506_04359_b200.shard import TrackGather
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -295,8 +296,7 @@ def main():
     side = torch.cuda.Stream(device=dev) if world > 1 else None
     pos_buf = [torch.zeros((B, P, 2), device=dev) for _ in range(2)]
     st_buf = [torch.zeros((B, P), dtype=torch.uint8, device=dev) for _ in range(2)]
-    gathered_pos = [torch.empty((world * B, P, 2), device=dev) for _ in range(2)] if world > 1 else None
-    gathered_st = [torch.empty((world * B, P), dtype=torch.uint8, device=dev) for _ in range(2)] if world > 1 else None
+    gathers = [TrackGather(B, P, dev) for _ in range(2)] if world > 1 else None
     gather_done = [None, None]
 
     n_total = args.warmup + args.steps
@@ -320,8 +320,7 @@ def main():
             done.record()
             with torch.cuda.stream(side):
                 side.wait_event(done)
-                dist.all_gather_into_tensor(gathered_pos[slot], pos_buf[slot])
-                dist.all_gather_into_tensor(gathered_st[slot], st_buf[slot])
+                gathers[slot].gather(pos_buf[slot], st_buf[slot])
                 e = torch.cuda.Event()
                 e.record(side)
                 gather_done[slot] = e
@@ -420,10 +419,17 @@ def main():
         "peaks": pk,
         "clocks": clock_rec,
     }
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = run_e2e(fe, stream.frames, sched, args, dev, F, C)
-    elif rank == 0:
-        line["e2e"] = None
+    if not args.no_e2e:
+        e2e = run_e2e(fe, stream.frames, sched, args, dev, F, C)
+        t = torch.tensor([e2e["ms"]], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.barrier()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+        line["e2e"] = {"value": world * B * args.steps / (ms_e2e / 1e3), "unit": "camera-frames/s",
+                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                       "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                       "ms_per_step": ms_e2e / args.steps}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ob = time_oracle(wl, args.cpu_seconds)
         line["cpu_baseline"] = {
@@ -490,9 +496,7 @@ def run_e2e(fe, ring, sched, args, dev, F, C):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
-    return {"value": B * args.steps / (ms / 1e3), "unit": "camera-frames/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": ms / args.steps}
+    return {"ms": ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
 if __name__ == "__main__":

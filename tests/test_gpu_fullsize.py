@@ -1,0 +1,101 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (device ring, pointer tables, B = F*C camera-frames per launch, the
+Frontend2D step): sampled outputs are recomputed by the oracle on the same
+bytes — pyramid rows, whole grid cells of the selection, and tracks of sampled
+keypoints — under the same bars as tests/test_gpu_parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle.parity import compare_klt
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import Frontend2D, RingSchedule
+
+
+def _setup(name, F=None, ring=None):
+    wl = synth.WORKLOADS[name]
+    C = wl.cams
+    F = F or max(1, 32 // C)
+    ring = ring or 2 * F
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    st = synth.make_stream(wl, ring, "cuda")
+    fe = Frontend2D(cfg, C, F, "cuda", wl.pitch)
+    sched = RingSchedule(st.frames, F)
+    fe.prime(sched.before_first, 1)
+    slot0 = fe.kp_xy[0].clone()  # keypoints of frame -1 (the carry overwrites slot 0)
+    cur, prev, parity = sched.tables(0)
+    fe.step(cur, prev, parity)
+    torch.cuda.synchronize()
+    fe.tracked_pts = torch.cat([slot0[None], fe.kp_xy[1:-1]], 0)  # [F, C, P, 2]
+    return wl, st, fe, sched, F
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_fullsize_sampled_parity(name):
+    wl, st, fe, sched, F = _setup(name)
+    C = wl.cams
+    rng = np.random.default_rng(sum(name.encode()))
+    frames = st.frames.cpu().numpy()
+    B = F * C
+    lay = fe.layout
+    samples = sorted(set(rng.choice(B, size=min(2, B), replace=False).tolist()) | {B - 1})
+    for b in samples:
+        f, c = divmod(b, C)
+        cur = frames[c, f % frames.shape[1], :, :wl.W]
+        prv = frames[c, (f - 1) % frames.shape[1], :, :wl.W]
+        # --- pyramid: sampled rows of every level, bit-exact
+        planes, dense_cur = oracle.build_pyramid(cur, wl.levels)
+        pyr = fe.pyr[0][b].cpu().numpy()
+        for L in range(1, wl.levels):
+            g = pyr[lay.offset[L]:lay.offset[L] + lay.pitch[L] * lay.H[L]].reshape(
+                lay.H[L], lay.pitch[L])[:, :lay.W[L]]
+            rows = rng.choice(lay.H[L], size=min(6, lay.H[L]), replace=False)
+            assert np.array_equal(g[rows].astype(np.float64), planes[L][rows]), (name, b, L)
+        # --- selection: whole sampled cells, bit-exact
+        oxy, osc, ocnt = oracle.detect_gftt(cur, wl.grid_x, wl.grid_y, k=wl.k, K_min=wl.K_min,
+                                            border=wl.border)
+        gxy = fe.kp_xy[1 + f, c].cpu().numpy().reshape(oxy.shape)
+        gsc = fe.kp_score[1 + f, c].cpu().numpy().reshape(osc.shape)
+        gcnt = fe.cell_count[1 + f, c].cpu().numpy()
+        assert np.array_equal(gcnt, ocnt), (name, b)
+        assert np.array_equal(gxy, oxy) and np.array_equal(gsc, osc), (name, b)
+        # --- KLT: sampled keypoints of the previous frame tracked prv -> cur
+        _, dense_prv = oracle.build_pyramid(prv, wl.levels)
+        pts_all = fe.tracked_pts[f, c].cpu().numpy().reshape(-1, 2)
+        valid = np.nonzero(pts_all[:, 0] >= 0)[0]
+        pick = rng.choice(valid, size=min(96, len(valid)), replace=False)
+        opos, ost, onc, dg = oracle.track_klt(dense_prv, dense_cur, wl.W, wl.H, wl.levels,
+                                              pts_all[pick], win=wl.win, iters=wl.iters,
+                                              eps=wl.eps, ncc_min=wl.ncc_min, min_eig=wl.min_eig)
+        gpos = fe.pos[b].cpu().numpy()[pick]
+        gst = fe.status[b].cpu().numpy()[pick]
+        stats = compare_klt(pts_all[pick], gpos, gst, opos, ost, dg)
+        assert stats["both_tracked"] > 0.5 * len(pick), stats
+
+
+def test_fullsize_tracking_quality_c2():
+    """Property at full size: tracked displacements match the generator's true
+    motion (Catmull-Rom rendering, so within ~0.1 px) for most tracks."""
+    wl, st, fe, sched, F = _setup("c2")
+    C = wl.cams
+    pos = fe.pos.cpu().numpy()
+    status = fe.status.cpu().numpy()
+    pts = fe.tracked_pts.cpu().numpy().reshape(F * C, -1, 2)
+    errs = []
+    for b in range(F * C):
+        f, c = divmod(b, C)
+        true = st.true_displacement(c, f)
+        ok = status[b] == 0
+        errs.append(np.abs(pos[b][ok] - pts[b][ok] - true).max(axis=1))
+    e = np.concatenate(errs)
+    assert len(e) > 0.8 * F * C * fe.P * 0.5
+    assert np.median(e) < 0.05 and np.mean(e < 0.2) > 0.95
