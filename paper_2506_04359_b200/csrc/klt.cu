@@ -71,44 +71,53 @@ __device__ __forceinline__ float2 warp_sum2(float2 v) {
 }
 
 // Stage rows [oy, oy+nr) x columns [ox, ox+32) of a level (clamp-to-edge)
-// into a warp patch, minus `shift` (lane = column).  Out of line and only
-// lightly unrolled: the kernel is instruction-cache bound, staging is not.
-template <typename T>
-__device__ __noinline__ void stage_t(float* __restrict__ sp, const T* __restrict__ base,
-                                     int64_t pitch, int W, int H, int ox, int oy, int nr,
-                                     float shift) {
+// into a warp patch (lane = column).  fp32 levels use cp.async (LDGSTS: every
+// row in flight at once, no registers); the u8 L0 frame is loaded 8 rows deep
+// and converted.  Out of line: the kernel is instruction-cache bound.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __noinline__ void stage_f32(float* __restrict__ sp, const float* __restrict__ base,
+                                       int64_t pitch, int W, int H, int ox, int oy, int nr) {
   const int lane = threadIdx.x & 31;
-  const T* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
+  const float* col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
   if (oy >= 0 && oy + nr <= H) {
-    const T* __restrict__ p = col + (int64_t)oy * pitch;
-    int r = 0;
-    for (; r + 4 <= nr; r += 4, p += 4 * pitch) {
-      const float v0 = (float)__ldg(p), v1 = (float)__ldg(p + pitch);
-      const float v2 = (float)__ldg(p + 2 * pitch), v3 = (float)__ldg(p + 3 * pitch);
-      sp[r * kPitch + lane] = v0 - shift;
-      sp[(r + 1) * kPitch + lane] = v1 - shift;
-      sp[(r + 2) * kPitch + lane] = v2 - shift;
-      sp[(r + 3) * kPitch + lane] = v3 - shift;
-    }
-    for (; r < nr; ++r, p += pitch) sp[r * kPitch + lane] = (float)__ldg(p) - shift;
+    const float* p = col + (int64_t)oy * pitch;
+    for (int r = 0; r < nr; ++r, p += pitch) cp_async4(sp + r * kPitch + lane, p);
   } else {
-    for (int r = 0; r < nr; ++r) {
-      const int y = clampi(oy + r, 0, H - 1);
-      sp[r * kPitch + lane] = (float)__ldg(col + (int64_t)y * pitch) - shift;
-    }
+    for (int r = 0; r < nr; ++r)
+      cp_async4(sp + r * kPitch + lane, col + (int64_t)clampi(oy + r, 0, H - 1) * pitch);
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncwarp();
+}
+
+__device__ __noinline__ void stage_u8(float* __restrict__ sp, const uint8_t* __restrict__ base,
+                                      int64_t pitch, int W, int H, int ox, int oy, int nr) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
+  __syncwarp();
+  for (int r0 = 0; r0 < nr; r0 += 8) {
+    unsigned v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      v[i] = r0 + i < nr ? __ldg(col + (int64_t)clampi(oy + r0 + i, 0, H - 1) * pitch) : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (r0 + i < nr) sp[(r0 + i) * kPitch + lane] = (float)v[i];
   }
   __syncwarp();
 }
 
 __device__ __forceinline__ void stage(float* __restrict__ sp, const Plane& pl, int ox, int oy,
-                                      int nr, float shift) {
+                                      int nr) {
   if (pl.u8)
-    stage_t<uint8_t>(sp, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy,
-                     nr, shift);
+    stage_u8(sp, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
   else
-    stage_t<float>(sp, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr,
-                   shift);
+    stage_f32(sp, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
 }
 
 struct LevelOut {
@@ -232,8 +241,8 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
   }
 }
 
-// sum over the window of e*(Tx, Ty), e = T' - S' (S' bilinear of the centred,
-// staged next-level patch at origin (lc0, lr0) with weights (bx, by)).
+// sum over the window of e*(Tx, Ty), e = T - S (S bilinear of the staged
+// next-level patch at origin (lc0, lr0) with weights (bx, by)).
 template <int WIN>
 __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, int lr0, float bx,
                                          float by, const Tmpl<WIN>& t) {
@@ -259,15 +268,16 @@ __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, 
   return f2(ax.x + ax.y, ay.x + ay.y);
 }
 
-// NCC moments (sum S', sum S'^2, sum T'S') of the centred patches.
+// NCC moments (sum S', sum S'^2, sum T'S') with S' = S - m, T' = T - m,
+// m = template mean (second pass of the two-pass NCC).
 template <int WIN>
 __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int lc0, int lr0,
-                                              float bx, float by, const Tmpl<WIN>& t) {
+                                              float bx, float by, float m, const Tmpl<WIN>& t) {
   constexpr int H2 = Tmpl<WIN>::H2;
   const int lane = threadIdx.x & 31;
   const float valid = lane < WIN ? 1.0f : 0.0f;
   const float* base = JP + lr0 * kPitch + lc0 + min(lane, WIN - 1);
-  const float2 wx = f2(bx, bx), wy = f2(by, by);
+  const float2 wx = f2(bx, bx), wy = f2(by, by), mm = f2(m, m);
   auto hrow = [&](int ra, int rb) {
     const float2 a0 = f2(base[ra * kPitch], base[rb * kPitch]);
     const float2 a1 = f2(base[ra * kPitch + 1], base[rb * kPitch + 1]);
@@ -278,11 +288,11 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
 #pragma unroll
   for (int p = 0; p < H2; ++p) {
     const float2 hn = hrow(p + 1, p + H2);
-    const float2 m = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
-    const float2 S = mul2(fma2(wy, sub2(hn, h), h), m);
+    const float2 msk = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
+    const float2 S = mul2(sub2(fma2(wy, sub2(hn, h), h), mm), msk);
     s1 = add2(s1, S);
     s2 = fma2(S, S, s2);
-    st = fma2(t.T[p], S, st);
+    st = fma2(sub2(t.T[p], mm), S, st);
     h = hn;
   }
   return make_float3(s1.x + s1.y, s2.x + s2.y, st.x + st.y);
@@ -308,7 +318,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   {
     const float fcx = floorf(cx), fcy = floorf(cy);
     const int ix = (int)fcx, iy = (int)fcy;
-    stage(sp, I, ix - R - 1, iy - R - 1, WIN + 3, 0.0f);
+    stage(sp, I, ix - R - 1, iy - R - 1, WIN + 3);
     build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, t);
   }
   out.levels++;
@@ -340,19 +350,19 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   }
   const float inv_det = 1.0f / det;
   const float i00 = gyy * inv_det, i01 = -gxy * inv_det, i11 = gxx * inv_det;
-  // centre the template: T' = T - mean (two-pass NCC; conditions e = T' - S')
-  const float tmean = g2s.y / (float)N;
+  // two-pass NCC, first pass: template mean, then sum (T - mean)^2 (T itself
+  // stays uncentred: the Gauss-Newton residual e = T - S needs no centring)
+  const float tmean = g2s.y * (1.0f / (float)N);
   const float valid = lane < WIN ? 1.0f : 0.0f;
-  float2 q = f2(0.f, 0.f);  // (sum T'^2, sum T')
+  float2 q = f2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < H2; ++p) {
     const float2 m = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
-    t.T[p] = mul2(sub2(t.T[p], f2(tmean, tmean)), m);
-    q = fma2(f2(t.T[p].x, 1.f), f2(t.T[p].x, t.T[p].x), q);
-    q = fma2(f2(t.T[p].y, 1.f), f2(t.T[p].y, t.T[p].y), q);
+    const float2 d = mul2(sub2(t.T[p], f2(tmean, tmean)), m);
+    q = fma2(d, d, q);
   }
-  q = warp_sum2(q);
-  const float Stt = q.x - q.y * q.y * (1.0f / (float)N);  // sum (T - mean)^2
+  const float2 qs = warp_sum2(q);
+  const float Stt = qs.x + qs.y;
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
   const int W = J.W, H = J.H;
@@ -368,7 +378,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     if (!staged || lc0 < 0 || lc0 > 2 * M || lr0 < 0 || lr0 > 2 * M) {
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
-      stage(sp, J, jx0, jy0, SZ, tmean);
+      stage(sp, J, jx0, jy0, SZ);
       staged = true;
       lc0 = M;
       lr0 = M;
@@ -403,14 +413,13 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
-    const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, t);
+    const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, tmean, t);
     const float2 r1 = warp_sum2(f2(mo.x, mo.y));
     const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
-    // two-pass NCC: T' = T - mean is centred; S' = S - mean_T, so
-    // sum(S-Sm)^2 = sum S'^2 - (sum S')^2/n and sum(T-Tm)(S-Sm) = sum T'S'
-    // - (sum T')(sum S')/n with sum T' ~ 0
+    // S' = S - mean_T: sum(S-Sm)^2 = sum S'^2 - (sum S')^2/n and
+    // sum(T-Tm)(S-Sm) = sum T'S' (sum T' = 0 up to rounding of the mean)
     const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
-    const float Sts = r2 - q.y * r1.x * (1.0f / (float)N);
+    const float Sts = r2;
     const float den2 = Stt * Sss;
     out.ncc = den2 > 0.0f ? Sts * rsqrtf(den2) : 0.0f;
     if (out.ncc < a.ncc_min) {
