@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--extras", action="store_true",
+                    help="also time the SURVEY §8(f) variants on the last step's data")
     return ap.parse_args()
 
 
@@ -419,6 +421,8 @@ def main():
         "peaks": pk,
         "clocks": clock_rec,
     }
+    if args.extras and rank == 0:
+        line["variants"] = run_variants(fe, sched, args, wl, F, C)
     if not args.no_e2e:
         e2e = run_e2e(fe, stream.frames, sched, args, dev, F, C)
         t = torch.tensor([e2e["ms"]], device=dev, dtype=torch.float64)
@@ -445,6 +449,72 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_variants(fe, sched, args, wl, F, C, reps=20):
+    """SURVEY §8(f) rows on the last timed step's data: f3 (11x11 window; NCC at
+    every Gauss-Newton step), f2 (cross-camera L->R tracking of stereo pairs with a
+    disparity prior), f4 (9x9 patches on every level).  Mean CUDA-event time per
+    launch and the kernel's own outputs summarised."""
+    import torch
+
+    from paper_2506_04359_b200 import vslam2d as v2d
+    c = fe.cfg
+    s = args.warmup + args.steps - 1
+    cur, prev, parity = sched.tables(s)
+    pyr_cur, pyr_prev = fe.pyr_ptrs[parity], fe.prev_pyr_ptrs[parity]
+    B, P = fe.B, fe.P
+    pts = fe.kp_xy[:-1].clone()           # what the step tracked (slot 0 = carried frame)
+    pos = torch.empty_like(fe.pos)
+    st = torch.empty_like(fe.status)
+    it = torch.empty_like(fe.iters)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    out = {}
+    for name, win, flags in (("klt_win11", 11, 0), ("klt_ncc_each_step", c.win, 1)):
+        ms = timed(lambda: v2d.track_klt_ptrs(prev, pyr_prev, cur, pyr_cur, fe.pitch, B, c.W, c.H,
+                                              c.levels, pts, None, None, P, win, c.iters, c.eps,
+                                              c.ncc_min, c.min_eig, pos, st, None, it, flags))
+        out[name] = {"ms_per_launch": ms, "camera_frames": B,
+                     "tracked_fraction": float((st == 0).sum()) / max(1, int((st != 4).sum())),
+                     "gn_steps_per_kp": float((it & 0xFFFFFF).sum()) / max(1, int((st != 4).sum()))}
+    if C >= 2 and wl.stereo_disparity > 0:
+        idx = torch.tensor([f * C + 2 * i for f in range(F) for i in range(C // 2)],
+                           device=cur.device)
+        src, dst = cur[idx], cur[idx + 1]
+        psrc, pdst = pyr_cur[idx], pyr_cur[idx + 1]
+        spts = fe.kp_xy[1:].reshape(B, P, 2)[idx].contiguous()
+        Bp = idx.numel()
+        guess = torch.tensor([-0.9 * wl.stereo_disparity, 0.0], device=cur.device)
+        guess = guess.view(1, 1, 2).expand(Bp, P, 2).contiguous()
+        cpos = torch.empty((Bp, P, 2), device=cur.device)
+        cst = torch.empty((Bp, P), dtype=torch.uint8, device=cur.device)
+        ms = timed(lambda: v2d.track_klt_ptrs(src, psrc, dst, pdst, fe.pitch, Bp, c.W, c.H,
+                                              c.levels, spts, guess, None, P, c.win, c.iters,
+                                              c.eps, c.ncc_min, c.min_eig, cpos, cst))
+        ok = cst == 0
+        err = (cpos - spts)[..., 0][ok] + wl.stereo_disparity
+        out["cross_camera_f2"] = {"ms_per_launch": ms, "stereo_pairs": Bp,
+                                  "tracked_fraction": float(ok.sum()) / max(1, int((cst != 4).sum())),
+                                  "median_abs_disparity_error_px": float(err.abs().median()) if ok.any() else None}
+    npatch = 9
+    pout = torch.empty((B, P, c.levels, npatch, npatch), device=cur.device)
+    kp = fe.kp_xy[1:].reshape(B, P, 2).contiguous()
+    ms = timed(lambda: v2d.extract_patches_ptrs(cur, pyr_cur, fe.pitch, B, c.W, c.H, c.levels, kp,
+                                                P, npatch, pout))
+    out["patches_f4"] = {"ms_per_launch": ms, "keypoints": B * P, "patch": npatch,
+                         "out_GBps": pout.numel() * 4 / (ms * 1e-3) / 1e9}
+    return out
 
 
 def run_e2e(fe, ring, sched, args, dev, F, C):

@@ -51,6 +51,10 @@ typedef struct CUstream_st* v2d_stream_t; /* identical to cudaStream_t */
 #define V2D_LOST_SMALL_EIG 3 /* lambda_min(G)/n < min_eig at level 0 */
 #define V2D_SKIPPED 4        /* input slot empty (-1,-1) / non-finite, or in_status != 0 */
 
+/* v2d_track_klt flags */
+#define V2D_KLT_NCC_EACH_STEP 1u /* variant f3: NCC gate also after every Gauss-Newton update
+                                    (literal "at each optimization step") */
+
 /* Pyramid layout of ONE image's levels 1..levels-1 (level 0 is the caller's u8
  * frame).  Level L (L >= 1) is a dense fp32 plane of W[L] x H[L] with row pitch
  * pitch[L] = round_up(W[L], 32) floats (128-B rows), at float offset offset[L]
@@ -119,13 +123,27 @@ int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int 
  *   iters_out  nullable [B][P] int32 work counters: bits 0..23 = Gauss-Newton
  *              steps over all levels, bits 24..31 = levels whose template was built
  * min_eig is in (gray/px)^2 per window pixel: lost at L0 when lambda_min(G)/n
- * < min_eig; coarse levels are skipped instead (reading #15). */
+ * < min_eig; coarse levels are skipped instead (reading #15).
+ * flags: 0 or V2D_KLT_NCC_EACH_STEP; unknown bits -> V2D_EINVAL. */
 int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_pyr_ptrs,
                   const uint8_t* const* next_l0_ptrs, const float* const* next_pyr_ptrs,
                   int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                   const float* guess, const uint8_t* in_status, int P, int win, int iters,
                   float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
-                  float* ncc, int32_t* iters_out, v2d_stream_t stream);
+                  float* ncc, int32_t* iters_out, unsigned flags, v2d_stream_t stream);
+
+/* Per-level patch features (variant f4; "a list of 9x9 image
+ * patches taken from each level of the image pyramid").  For
+ * every keypoint p of image b and every level L, the patch x patch samples
+ * S(I_L, c_L + (u, v)), u, v in [-(patch-1)/2, (patch-1)/2], c_L = (p+0.5)/2^L - 0.5
+ * (reading #2), bilinear with clamp-to-edge (D2), of the frame whose level 0 is
+ * l0_ptrs[b] and levels >= 1 pyr_ptrs[b].
+ *   pts   [B][P][2] fp32 L0 px; empty slots (-1,-1) / non-finite -> all-zero patches
+ *   out   [B][P][levels][patch][patch] fp32
+ * V2D_EINVAL: patch even, < 1 or > 31; bad levels / sizes. */
+int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs,
+                        int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
+                        int P, int patch, float* out, v2d_stream_t stream);
 
 /* Static string for a V2D_* return code. */
 const char* v2d_strerror(int code);

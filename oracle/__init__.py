@@ -61,7 +61,8 @@ def lib() -> ctypes.CDLL:
         L.v2dref_detect_gftt.argtypes = [P, i64, i, i, i, i, i, i, f, i, i, P, P, P]
         L.v2dref_ncc.argtypes = [P, P, i]
         L.v2dref_ncc.restype = d
-        L.v2dref_track_klt.argtypes = [P, P, i, i, i, P, P, P, i, i, i, d, d, d, P, P, P, P]
+        L.v2dref_track_klt.argtypes = [P, P, i, i, i, P, P, P, i, i, i, d, d, d, i, P, P, P, P]
+        L.v2dref_extract_patches.argtypes = [P, i, i, i, P, i, i, P]
         _lib = L
     return _lib
 
@@ -165,7 +166,8 @@ def ncc(P: np.ndarray, Q: np.ndarray) -> float:
 def track_klt(prev_dense: np.ndarray, next_dense: np.ndarray, W: int, H: int, levels: int,
               pts: np.ndarray, guess: np.ndarray | None = None,
               in_status: np.ndarray | None = None, win: int = 21, iters: int = 10,
-              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01):
+              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01,
+              ncc_each_step: bool = False):
     """D7.  prev_dense/next_dense: dense float64 pyramids from build_pyramid()[1].
     Returns (pos float64 [P,2], status uint8 [P], ncc float64 [P], diag float64 [P,4])."""
     pts = np.ascontiguousarray(pts, dtype=np.float32).reshape(-1, 2)
@@ -178,6 +180,17 @@ def track_klt(prev_dense: np.ndarray, next_dense: np.ndarray, W: int, H: int, le
     dg = np.zeros((P, 4), np.float64)
     _check(lib().v2dref_track_klt(_ptr(prev_dense), _ptr(next_dense), W, H, levels, _ptr(pts),
                                   _ptr(g), _ptr(s_in), P, win, iters, float(eps), float(ncc_min),
-                                  float(min_eig), _ptr(pos), _ptr(st), _ptr(nc), _ptr(dg)),
+                                  float(min_eig), int(ncc_each_step), _ptr(pos), _ptr(st),
+                                  _ptr(nc), _ptr(dg)),
            "track_klt")
     return pos, st, nc, dg
+
+
+def extract_patches(dense_pyr: np.ndarray, W: int, H: int, levels: int, pts: np.ndarray,
+                    patch: int = 9):
+    """Variant f4: float64 [P, levels, patch, patch]."""
+    pts = np.ascontiguousarray(pts, dtype=np.float32).reshape(-1, 2)
+    out = np.zeros((pts.shape[0], levels, patch, patch), np.float64)
+    _check(lib().v2dref_extract_patches(_ptr(dense_pyr), W, H, levels, _ptr(pts), pts.shape[0],
+                                        patch, _ptr(out)), "extract_patches")
+    return out

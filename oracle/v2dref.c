@@ -323,7 +323,7 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
                      const float* pts, const float* guess,
                      const uint8_t* in_status, int P,
                      int win, int iters, double eps, double ncc_min,
-                     double min_eig,
+                     double min_eig, int ncc_each_step,
                      double* out_pos, uint8_t* status, double* ncc,
                      double* diag) {
   int Ws[8], Hs[8];
@@ -425,6 +425,17 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
           st = V2DREF_LOST_OOB;
           break;
         }
+        if (ncc_each_step) { /* variant f3: NCC after every optimization step */
+          for (int v = -r, i = 0; v <= r; ++v)
+            for (int u = -r; u <= r; ++u, ++i)
+              S[i] = v2dref_bilinear(J[L], wl, hl, cx + dx + u, cy + dy + v);
+          last_ncc = v2dref_ncc(T, S, n);
+          m_ncc = dmin(m_ncc, fabs(last_ncc - ncc_min));
+          if (last_ncc < ncc_min) {
+            st = V2DREF_LOST_NCC;
+            break;
+          }
+        }
         double step = sqrt(ex * ex + ey * ey);
         m_eps = dmin(m_eps, fabs(step - eps));
         if (step < eps) break; /* reading #12 */
@@ -476,5 +487,32 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
   free(TX);
   free(TY);
   free(S);
+  return V2DREF_OK;
+}
+
+/* ------------------------------------------------------- f4 patches ---- */
+/* "a list of 9x9 image patches taken from each level of the image pyramid"
+ * (P:216); sampled like the KLT template (D2, reading #2). */
+int v2dref_extract_patches(const double* pyr, int W, int H, int levels, const float* pts, int P,
+                           int patch, double* out) {
+  int Ws[8], Hs[8];
+  if (!pyr || (P > 0 && (!pts || !out)) || patch < 1 || (patch % 2) == 0) return V2DREF_EINVAL;
+  if (v2dref_level_dims(W, H, levels, Ws, Hs) != V2DREF_OK) return V2DREF_EINVAL;
+  const int r = (patch - 1) / 2, n = patch * patch;
+  for (int p = 0; p < P; ++p) {
+    double px = pts[2 * p], py = pts[2 * p + 1];
+    int empty = (px == -1.0 && py == -1.0) || !isfinite(px) || !isfinite(py);
+    int64_t off = 0;
+    for (int L = 0; L < levels; ++L) {
+      const double* I = pyr + off;
+      double scale = (double)(1 << L);
+      double cx = (px + 0.5) / scale - 0.5, cy = (py + 0.5) / scale - 0.5;
+      for (int v = 0; v < patch; ++v)
+        for (int u = 0; u < patch; ++u)
+          out[((int64_t)p * levels + L) * n + v * patch + u] =
+              empty ? 0.0 : v2dref_bilinear(I, Ws[L], Hs[L], cx + (u - r), cy + (v - r));
+      off += (int64_t)Ws[L] * Hs[L];
+    }
+  }
   return V2DREF_OK;
 }

@@ -84,6 +84,9 @@ double v2dref_ncc(const double* P, const double* Q, int n);
 /* D7: pyramidal forward-additive LK with template gradients and a per-level
  * NCC gate.  prev_pyr / next_pyr are dense pyramids from
  * v2dref_build_pyramid of the same W x H and level count.
+ * ncc_each_step != 0 selects the literal reading of P:61 ("NCC check at each
+ * optimization step", variant f3 / DESIGN.md reading #13): the NCC gate is
+ * also applied after every Gauss-Newton update, not only after each level.
  * pts [P][2] (L0 px; (-1,-1) = empty slot), guess [P][2] nullable (L0 px
  * displacement prior), in_status [P] nullable (non-zero = already lost).
  * Outputs: out_pos [P][2] (float64; (-1,-1) unless TRACKED), status [P],
@@ -99,9 +102,15 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
                      const float* pts, const float* guess,
                      const uint8_t* in_status, int P,
                      int win, int iters, double eps, double ncc_min,
-                     double min_eig,
+                     double min_eig, int ncc_each_step,
                      double* out_pos, uint8_t* status, double* ncc,
                      double* diag);
+
+/* Variant f4: patch x patch bilinear samples of every level at
+ * c_L + (u, v), c_L = (p+0.5)/2^L - 0.5; out [P][levels][patch][patch];
+ * empty slots (-1,-1) give zeros.  pyr: dense pyramid of v2dref_build_pyramid. */
+int v2dref_extract_patches(const double* pyr, int W, int H, int levels, const float* pts, int P,
+                           int patch, double* out);
 
 #ifdef __cplusplus
 }

@@ -110,8 +110,9 @@ int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_p
                   int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                   const float* guess, const uint8_t* in_status, int P, int win, int iters,
                   float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
-                  float* ncc, int32_t* iters_out, v2d_stream_t stream) {
+                  float* ncc, int32_t* iters_out, unsigned flags, v2d_stream_t stream) {
   v2d::Levels lv;
+  if (flags & ~V2D_KLT_NCC_EACH_STEP) return V2D_EINVAL;
   if (B < 0 || P < 0) return V2D_EINVAL;
   if ((int64_t)B * P > ((int64_t)1 << 40)) return V2D_EINVAL;
   if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
@@ -121,10 +122,23 @@ int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_p
     return V2D_EINVAL;
   if ((int64_t)B * P > 0 && levels > 1 && (!prev_pyr_ptrs || !next_pyr_ptrs)) return V2D_EINVAL;
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
-  v2d::KltArgs a{W, H, P, win, iters, eps, ncc_min, min_eig, l0_pitch};
+  v2d::KltArgs a{W, H, P, win, iters, eps, ncc_min, min_eig, l0_pitch, flags};
   return v2d::launch_klt(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, B, lv, a, pts,
                          guess, in_status, out_pos, status, ncc, iters_out,
                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs,
+                        int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
+                        int P, int patch, float* out, v2d_stream_t stream) {
+  v2d::Levels lv;
+  if (B < 0 || P < 0 || patch < 1 || patch > 31 || (patch % 2) == 0) return V2D_EINVAL;
+  if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
+  if ((int64_t)B * P > 0 && (!l0_ptrs || !pts || !out || (levels > 1 && !pyr_ptrs)))
+    return V2D_EINVAL;
+  if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
+  return v2d::launch_patches(l0_ptrs, pyr_ptrs, l0_pitch, B, lv, pts, P, patch, out,
+                             reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

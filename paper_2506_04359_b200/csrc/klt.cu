@@ -406,6 +406,21 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
       out.status = V2D_LOST_OOB;
       return;
     }
+    if (a.flags & V2D_KLT_NCC_EACH_STEP) {  // variant f3: NCC after every update
+      int lc0n, lr0n;
+      float bxn, byn;
+      locate(nx, ny, lc0n, lr0n, bxn, byn);
+      const float3 mo = ncc_moments<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, t);
+      const float2 r1 = warp_sum2(f2(mo.x, mo.y));
+      const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
+      const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
+      const float den2 = Stt * Sss;
+      out.ncc = den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
+      if (out.ncc < a.ncc_min) {
+        out.status = V2D_LOST_NCC;
+        return;
+      }
+    }
     if (fmaf(ex, ex, ey * ey) < eps2) break;
   }
   // ---------------- per-level NCC gate --------------------------------------

@@ -81,7 +81,7 @@ class Frontend2D:
         v2d.track_klt_ptrs(prev_l0_ptrs, self.prev_pyr_ptrs[parity], l0_ptrs,
                            self.pyr_ptrs[parity], self.pitch, B, W, H, L, self.kp_xy[:-1],
                            None, None, self.P, c.win, c.iters, c.eps, c.ncc_min, c.min_eig,
-                           self.pos, st, self.ncc, self.iters)
+                           self.pos, st, self.ncc, self.iters, c.klt_flags)
         if events is not None:
             events[3].record()
         self.kp_xy[0].copy_(self.kp_xy[-1], non_blocking=True)

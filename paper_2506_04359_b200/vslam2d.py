@@ -21,6 +21,7 @@ from . import build as _build
 LIB_PATH = _build.LIB
 
 TRACKED, LOST_OOB, LOST_NCC, LOST_SMALL_EIG, SKIPPED = 0, 1, 2, 3, 4
+KLT_NCC_EACH_STEP = 1
 MAX_LEVELS, MAX_K, MAX_WIN = 8, 256, 29
 
 
@@ -35,7 +36,7 @@ class Layout(ctypes.Structure):
 
 
 _SYMBOLS = ("v2d_pyramid_layout", "v2d_grid_k", "v2d_build_pyramid", "v2d_detect_gftt",
-            "v2d_track_klt", "v2d_strerror", "v2d_version")
+            "v2d_track_klt", "v2d_extract_patches", "v2d_strerror", "v2d_version")
 
 _lib = None
 
@@ -55,7 +56,8 @@ def load() -> ctypes.CDLL:
     L.v2d_build_pyramid.argtypes = [vp, i64, i, i, i, i, vp, vp]
     L.v2d_detect_gftt.argtypes = [vp, i64, i, i, i, i, i, i, i, f, i, i, vp, vp, vp, vp, vp]
     L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
-                                vp, vp, vp, vp, vp]
+                                vp, vp, vp, vp, ctypes.c_uint, vp]
+    L.v2d_extract_patches.argtypes = [vp, vp, i64, i, i, i, i, vp, i, i, vp, vp]
     L.v2d_strerror.argtypes = [i]
     L.v2d_strerror.restype = ctypes.c_char_p
     L.v2d_version.restype = i
@@ -134,13 +136,13 @@ def detect_gftt_ptrs(l0_ptrs, l0_pitch, B, W, H, grid_x, grid_y, k, K_min, min_s
 
 def track_klt_ptrs(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, l0_pitch, B, W, H,
                    levels, pts, guess, in_status, P, win, iters, eps, ncc_min, min_eig, out_pos,
-                   status, ncc=None, iters_out=None):
+                   status, ncc=None, iters_out=None, flags=0):
     _need_cuda(pts, guess, in_status, out_pos, status, ncc, iters_out)
     _check(load().v2d_track_klt(_p(prev_l0_ptrs), _p(prev_pyr_ptrs), _p(next_l0_ptrs),
                                 _p(next_pyr_ptrs), l0_pitch, B, W, H, levels, _p(pts), _p(guess),
                                 _p(in_status), P, win, iters, float(eps), float(ncc_min),
                                 float(min_eig), _p(out_pos), _p(status), _p(ncc), _p(iters_out),
-                                _stream()), "track_klt")
+                                int(flags), _stream()), "track_klt")
 
 
 # --------------------------------------------------------------------------
@@ -183,7 +185,7 @@ def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int =
 
 def track_klt(prev_frames, prev_pyr, next_frames, next_pyr, W: int, levels: int,
               pts: torch.Tensor, guess=None, in_status=None, win: int = 21, iters: int = 10,
-              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01):
+              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01, flags: int = 0):
     """pts [B, P, 2] -> (pos [B,P,2], status u8 [B,P], ncc [B,P], iters int32 [B,P])."""
     B, H, pitch = _frames(prev_frames)
     _frames(next_frames)
@@ -198,7 +200,7 @@ def track_klt(prev_frames, prev_pyr, next_frames, next_pyr, W: int, levels: int,
                    ptrs_of(next_pyr), pitch, B, W, H, levels, pts,
                    None if guess is None else guess.contiguous().float(),
                    None if in_status is None else in_status.contiguous(), P, win, iters, eps,
-                   ncc_min, min_eig, pos, st, nc, it)
+                   ncc_min, min_eig, pos, st, nc, it, flags)
     return pos, st, nc, it
 
 
@@ -219,3 +221,31 @@ class FrontendConfig:
     eps: float = 0.01
     ncc_min: float = 0.8
     min_eig: float = 0.01
+    klt_flags: int = 0
+
+
+def extract_patches_ptrs(l0_ptrs, pyr_ptrs, l0_pitch, B, W, H, levels, pts, P, patch, out):
+    _need_cuda(pts, out)
+    _check(load().v2d_extract_patches(_p(l0_ptrs), _p(pyr_ptrs), l0_pitch, B, W, H, levels,
+                                      _p(pts), P, patch, _p(out), _stream()), "extract_patches")
+
+
+def extract_patches(frames, pyr, W: int, levels: int, pts: torch.Tensor, patch: int = 9):
+    """Variant f4: [B, P, levels, patch, patch] fp32 patches."""
+    B, H, pitch = _frames(frames)
+    P = pts.shape[1]
+    out = torch.empty((B, P, levels, patch, patch), dtype=torch.float32, device=pts.device)
+    extract_patches_ptrs(ptrs_of(frames), ptrs_of(pyr), pitch, B, W, H, levels,
+                         pts.contiguous().float(), P, patch, out)
+    return out
+
+
+def cross_camera_track(src_frames, src_pyr, dst_frames, dst_pyr, W: int, levels: int,
+                       pts: torch.Tensor, disparity_prior=(0.0, 0.0), **kw):
+    """Variant f2 ("cross-camera
+    (left-to-right) tracking"): the same pyramidal LK + NCC kernel between two
+    synchronized cameras, seeded with a disparity prior (dst = src + prior)."""
+    B, P = pts.shape[0], pts.shape[1]
+    guess = torch.tensor(disparity_prior, dtype=torch.float32, device=pts.device)
+    guess = guess.view(1, 1, 2).expand(B, P, 2).contiguous()
+    return track_klt(src_frames, src_pyr, dst_frames, dst_pyr, W, levels, pts, guess=guess, **kw)

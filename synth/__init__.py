@@ -64,6 +64,7 @@ class Workload:
     motion: tuple = (6.0, 0.0)    # max per-frame |dx|, |dy| (px)
     frames: int = 1000
     fixed_motion: tuple | None = None
+    stereo_disparity: float = 20.0  # odd camera = even camera's plane seen 20 px to the left
     description: str = ""
 
     @property
@@ -204,24 +205,36 @@ class Stream:
 
 
 def make_stream(wl: Workload, ring: int, device="cpu", cams: list[int] | None = None,
-                rank_salt: int = 0, smooth: bool = False) -> Stream:
-    """Render `ring` frames for each camera in `cams` (default all)."""
+                 rank_salt: int = 0, smooth: bool = False) -> Stream:
+    """Render `ring` frames for each camera in `cams` (default all).  Cameras
+    (2i, 2i+1) form rectified stereo pairs when wl.stereo_disparity > 0: the
+    right camera renders the left camera's texture and trajectory shifted by the
+    disparity (a fronto-parallel plane), so cross-camera tracking (f2) has a
+    known answer; all other cameras are independent."""
     cams = list(range(wl.cams)) if cams is None else cams
     frames = torch.zeros((len(cams), ring, wl.H, wl.pitch), dtype=torch.uint8, device=device)
     offs = np.zeros((len(cams), ring, 2))
+    tex_cache = {}
     for ci, c in enumerate(cams):
-        seed = seed_for(wl.index, c, rank_salt)
+        stereo_right = wl.stereo_disparity > 0 and (c % 2 == 1)
+        src = c - 1 if stereo_right else c
+        seed = seed_for(wl.index, src, rank_salt)
         if wl.fixed_motion is not None:
             o = np.zeros((ring, 2))
             for t in range(1, ring):
                 o[t] = o[t - 1] + np.asarray(wl.fixed_motion)
         else:
             o = trajectory(ring, wl.motion, seed)
-        span_x = int(math.ceil(np.abs(o[:, 0]).max())) + 4
+        disp = wl.stereo_disparity if wl.stereo_disparity > 0 else 0.0
+        span_x = int(math.ceil(np.abs(o[:, 0]).max() + disp)) + 4
         span_y = int(math.ceil(np.abs(o[:, 1]).max())) + 4
-        tex = make_texture(wl.H + 2 * span_y, wl.W + 2 * span_x, seed, device, smooth=smooth)
-        render(tex, o, wl.H, wl.W, wl.pitch, origin=(span_x, span_y), out=frames[ci])
-        offs[ci] = o
+        if src not in tex_cache:
+            tex_cache[src] = make_texture(wl.H + 2 * span_y, wl.W + 2 * span_x, seed, device,
+                                          smooth=smooth)
+        tex = tex_cache[src]
+        oo = o - np.array([disp, 0.0]) if stereo_right else o
+        render(tex, oo, wl.H, wl.W, wl.pitch, origin=(span_x, span_y), out=frames[ci])
+        offs[ci] = oo
     return Stream(frames, offs, wl)
 
 
@@ -240,3 +253,17 @@ def shifted_pair(H: int, W: int, shift: tuple[float, float], seed: int, smooth: 
     o = np.array([[0.0, 0.0], [sx, sy]])
     fr = render(tex, o, H, W, pitch or W, origin=(span, span))
     return fr[0].numpy(), fr[1].numpy()
+
+
+def stereo_pair(H: int, W: int, disparity: float, seed: int, smooth: bool = False,
+                occluder: tuple | None = None, pitch: int | None = None):
+    """Rectified stereo pair of a fronto-parallel textured plane: the right image
+    sees world point x at x - disparity (disparity = fx * b / z; SPEC S:179 uses
+    fx=400, b=0.1 m, z=2 m -> 20 px).  `occluder` = (x0, y0, w, h) paints a
+    uniform block into the right image only."""
+    left, right = shifted_pair(H, W, (-disparity, 0.0), seed, smooth=smooth, pitch=pitch)
+    if occluder is not None:
+        x0, y0, w, h = occluder
+        right = right.copy()
+        right[y0:y0 + h, x0:x0 + w] = 128
+    return left, right

@@ -88,13 +88,13 @@ def test_validation_without_gpu(v2d):
     args = dict(eps=0.01, ncc=0.8, eig=0.01)
     f = ctypes.c_float
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 20, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, N) == -1
+                           f(0.01), N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 31, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, N) == -1
+                           f(0.01), N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 21, 0, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, N) == -1
+                           f(0.01), N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 72, 0, 70, 64, 3, N, N, N, 0, 21, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, N) == -2
+                           f(0.01), N, N, N, N, 0, N) == -2
     # empty batches are valid no-ops (no CUDA call is made for B == 0)
     assert L.v2d_build_pyramid(N, 64, 0, 64, 64, 3, N, N) == 0
     assert L.v2d_strerror(-2).decode().startswith("pitch")

@@ -27,7 +27,7 @@ def _to_dev(frames_u8: np.ndarray, pitch: int | None = None):
 
 
 def _stream(W, H, n, seed, motion=(3.0, 2.0)):
-    wl = synth.Workload("t", 7, W, H, 1, 3, motion=motion)
+    wl = synth.Workload("t", 7, W, H, 1, 3, motion=motion, stereo_disparity=0.0)
     st = synth.make_stream(wl, n, "cpu", rank_salt=seed)
     return st.frames[0][:, :, :W].numpy().copy(), st
 
@@ -122,7 +122,7 @@ def test_detect_rejects_bad_k():
 
 # ---------------------------------------------------------------------- KLT
 def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in_status=None,
-              eps=0.01):
+              eps=0.01, each_step=False):
     B = fr_prev.shape[0]
     dp, dn = _to_dev(fr_prev), _to_dev(fr_next)
     pp = v2d.build_pyramid(dp, W, levels)
@@ -131,7 +131,8 @@ def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in
     tg = None if guess is None else torch.from_numpy(guess).cuda()
     ti = None if in_status is None else torch.from_numpy(in_status).cuda()
     pos, st, nc, it = v2d.track_klt(dp, pp, dn, pn, W, levels, tp, guess=tg, in_status=ti,
-                                    win=win, iters=iters, eps=eps)
+                                    win=win, iters=iters, eps=eps,
+                                    flags=v2d.KLT_NCC_EACH_STEP if each_step else 0)
     pos, st, nc = pos.cpu().numpy(), st.cpu().numpy(), nc.cpu().numpy()
     H = fr_prev.shape[1]
     stats = []
@@ -140,7 +141,8 @@ def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in
         _, d1 = oracle.build_pyramid(fr_next[b], levels)
         opos, ost, onc, dg = oracle.track_klt(
             d0, d1, W, H, levels, pts[b], guess=None if guess is None else guess[b],
-            in_status=None if in_status is None else in_status[b], win=win, iters=iters, eps=eps)
+            in_status=None if in_status is None else in_status[b], win=win, iters=iters, eps=eps,
+            ncc_each_step=each_step)
         stats.append(compare_klt(pts[b], pos[b], st[b], opos, ost, dg))
     return stats
 
@@ -192,3 +194,62 @@ def test_klt_noise_rejects():
     stats = _klt_case(fr, noise, W, 3, pts)
     valid = (pts[0, :, 0] >= 0).sum()
     assert stats[0]["status_hist_gpu"][0] <= 0.1 * valid
+
+
+@pytest.mark.parametrize("win", [21, 11])
+def test_klt_variant_ncc_each_step(win):
+    """Variant f3 (NCC gate after every Gauss-Newton update) vs the oracle."""
+    W, H = 320, 240
+    fr, _ = _stream(W, H, 3, 77 + win, motion=(4.0, 3.0))
+    prev, nxt = fr[:-1], fr[1:]
+    pts = np.stack([oracle.detect_gftt(f, 4, 4, k=16, border=(win - 1) // 2 + 1)[0].reshape(-1, 2)
+                    for f in prev])
+    stats = _klt_case(prev, nxt, W, 4, pts, win=win, each_step=True)
+    assert sum(s["both_tracked"] for s in stats) > 0.3 * pts.shape[0] * pts.shape[1]
+
+
+def test_klt_rejects_unknown_flags():
+    d = torch.zeros((1, 64, 64), dtype=torch.uint8, device="cuda")
+    p = v2d.build_pyramid(d, 64, 2)
+    with pytest.raises(v2d.V2DError):
+        v2d.track_klt(d, p, d, p, 64, 2, torch.zeros((1, 1, 2), device="cuda"), flags=2)
+
+
+# ------------------------------------------------------------ f4 patches
+@pytest.mark.parametrize("W,H,levels,patch", [(320, 240, 4, 9), (97, 61, 3, 9), (200, 150, 2, 5)])
+def test_patches_parity(W, H, levels, patch):
+    fr, _ = _stream(W, H, 2, W + patch)
+    d = _to_dev(fr)
+    pyr = v2d.build_pyramid(d, W, levels)
+    rng = np.random.default_rng(W)
+    pts = np.stack([np.concatenate([rng.uniform(0, [W - 1, H - 1], (40, 2)),
+                                    [[-1, -1], [0, 0], [W - 1, H - 1], [5.0, 7.0]]])
+                    for _ in range(2)]).astype(np.float32)
+    out = v2d.extract_patches(d, pyr, W, levels, torch.from_numpy(pts).cuda(), patch).cpu().numpy()
+    for b in range(2):
+        _, dense = oracle.build_pyramid(fr[b], levels)
+        ref = oracle.extract_patches(dense, W, H, levels, pts[b], patch)
+        # fp32 sample positions: |error| <= ulp(max(W,H)) in the bilinear weight,
+        # times the largest intensity step (255) + fp32 interpolation rounding
+        tol = 255 * float(np.spacing(np.float32(max(W, H)))) + 1e-4
+        assert np.abs(out[b] - ref).max() <= tol
+        ints = np.all(pts[b] == np.round(pts[b]), axis=1)
+        assert np.array_equal(out[b][ints, 0], ref[ints, 0].astype(np.float32))  # L0 exact
+
+
+# ------------------------------------------------------------ f2 stereo
+def test_cross_camera_parity():
+    """Variant f2: left -> right tracking with a disparity prior, vs the oracle."""
+    W, H = 320, 240
+    left, right = synth.stereo_pair(H, W, 20.0, seed=5, occluder=(100, 80, 60, 60))
+    pts = oracle.detect_gftt(left, 4, 4, k=12, border=11)[0].reshape(1, -1, 2)
+    guess = np.tile(np.array([[[-17.5, 0.5]]], np.float32), (1, pts.shape[1], 1))
+    stats = _klt_case(left[None], right[None], W, 3, pts, guess=guess)
+    assert stats[0]["both_tracked"] > 0.5 * pts.shape[1]
+    # the convenience API is the same kernel with the prior broadcast
+    dl, dr = _to_dev(left[None]), _to_dev(right[None])
+    pl, pr = v2d.build_pyramid(dl, W, 3), v2d.build_pyramid(dr, W, 3)
+    tp = torch.from_numpy(pts).cuda()
+    a = v2d.cross_camera_track(dl, pl, dr, pr, W, 3, tp, disparity_prior=(-17.5, 0.5))
+    b = v2d.track_klt(dl, pl, dr, pr, W, 3, tp, guess=torch.from_numpy(guess).cuda())
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])

@@ -177,3 +177,20 @@ def test_guess_prior_extends_range():
     ok = (st2 == oracle.TRACKED) & inner
     assert ok.mean() / inner.mean() > max(0.9, base)
     assert np.abs(pos2[ok] - pts[ok] - [36, 0]).max() < 0.01
+
+
+def test_ncc_each_step_variant_is_stricter():
+    """Variant f3 (NCC at every optimization step, literal P:61): it adds checks,
+    so its TRACKED set is a subset of the per-level reading's, with identical
+    positions where both track; on identical frames both agree exactly."""
+    for (f0, f1) in [synth.shifted_pair(H, W, (3.2, -1.7), seed=13),
+                     (_big(3)[M:M + H, M:M + W].copy(), synth.noise_frame(H, W, 5))]:
+        pts, (p0, s0, n0, d0) = _track(f0, f1, 3)
+        _, (p1, s1, n1, d1) = _track(f0, f1, 3, pts=pts, ncc_each_step=True)
+        t1 = s1 == oracle.TRACKED
+        assert np.all(s0[t1] == oracle.TRACKED)
+        assert np.array_equal(p1[t1], p0[t1])
+    f0 = _big(1)[M:M + H, M:M + W].copy()
+    pts, (p0, s0, _, _) = _track(f0, f0, 3)
+    _, (p1, s1, _, _) = _track(f0, f0, 3, pts=pts, ncc_each_step=True)
+    assert np.array_equal(s0, s1) and np.array_equal(p0, p1)

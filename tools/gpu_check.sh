@@ -3,7 +3,7 @@ mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
 timeout 900 python bench.py > gpurun_out/bench_c2.log 2>&1; echo bench=$?
-timeout 900 python bench.py --config c5 --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c5.log 2>&1; echo bench5=$?
+timeout 900 python bench.py --config c5 --steps 100 --warmup 5 --no-cpu-baseline --extras > gpurun_out/bench_c5.log 2>&1; echo bench5=$?
 if [ "$1" = "ncu" ]; then
   B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
   $B > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
