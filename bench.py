@@ -514,6 +514,29 @@ def run_variants(fe, sched, args, wl, F, C, reps=20):
                                                 P, npatch, pout))
     out["patches_f4"] = {"ms_per_launch": ms, "keypoints": B * P, "patch": npatch,
                          "out_GBps": pout.numel() * 4 / (ms * 1e-3) / 1e9}
+    # f1: keyframe-driven continuous tracking over the ring, one rig-frame per step
+    from paper_2506_04359_b200.frontend import KeyframeTracker
+    kt = KeyframeTracker(c, C, cur.device, fe.pitch, T=0.7)
+    ring_C = sched.C
+    frame_ptr = lambda t: sched.cur[(t // F) % sched.n_steps].view(F, ring_C)[t % F]
+    n_frames = min(60, sched.R - 1)
+    kt.start(frame_ptr(0))
+    kt.step(frame_ptr(1), frame_ptr(0))
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kfs = torch.zeros((), dtype=torch.int32, device=cur.device)
+    a.record()
+    for t in range(2, n_frames):
+        kt.step(frame_ptr(t), frame_ptr(t - 1))
+        kfs += kt.flag[0]
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / (n_frames - 2)
+    alive = float((kt.table()[1] == 0).float().mean())
+    out["keyframe_tracking_f1"] = {"ms_per_rig_frame": ms, "camera_frames_per_s": C / (ms * 1e-3),
+                                   "keyframe_rate": float(kfs.item()) / (n_frames - 2),
+                                   "alive_fraction_end": alive, "T": 0.7,
+                                   "min_separation_px": kt.min_sep, "launches_per_frame": 8}
     return out
 
 

@@ -100,11 +100,17 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
  *   cell_count [B][grid_y*grid_x]        int32 filled slots per cell
  *   resp       nullable [B][H][W] fp32: full R map (0 outside 2..W-3 x 2..H-3);
  *              when given, the lazy-eigenvalue shortcut is disabled.
+ *   mask_ptrs  nullable device array [B] of u8 masks (row pitch l0_pitch); a
+ *              non-zero mask pixel is not eligible (min_separation suppression,
+ *              S:158; NMS still compares against it)
+ *   enable     nullable device int32 flag; when *enable == 0 the call does
+ *              nothing (keyframe-conditional detection without a host sync)
  * V2D_EINVAL: border < 3, W or H < 2*border+1, grid cell < 1 px, bad k, nms not
  * 0/1, l0_pitch*H >= 2^31.  V2D_EALIGN: l0_pitch % 16 != 0. */
 int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
                     int grid_x, int grid_y, int k, int K_min, float min_score, int border,
                     int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
+                    const uint8_t* const* mask_ptrs, const int32_t* enable,
                     v2d_stream_t stream);
 
 /* Pyramidal LK tracking (LK_1981, LK_2000; reading of SURVEY §8(c) D7):
@@ -144,6 +150,41 @@ int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_p
 int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs,
                         int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                         int P, int patch, float* out, v2d_stream_t stream);
+
+/* ---- variant f1: keyframe-driven continuous tracking (Eq. 5;
+ * SPEC S:136-143).  A track table per image holds P slots:
+ * tracks [B][P][2] fp32, status [B][P] u8 (the KLT status codes: V2D_TRACKED =
+ * alive, anything else = lost; passing it back as v2d_track_klt's in_status makes
+ * lost terminal), kf_member [B][P] u8 (slot in S_kf), track_id [B][P]
+ * int32, next_id [B] int32.  A lost slot only becomes alive again through
+ * refill, with a new id. */
+
+/* mask(x,y) := 1 iff (x-tx)^2 + (y-ty)^2 < min_sep^2 for an alive track t of the
+ * image, else 0 (exact fp64 test).  mask_ptrs: device array [B] of u8 images,
+ * row pitch mask_pitch (% 16 == 0).  enable: nullable device flag (0 = skip). */
+int v2d_suppress_mask(const float* tracks, const uint8_t* status, int B, int P, float min_sep,
+                      int W, int H, uint8_t* const* mask_ptrs, int64_t mask_pitch,
+                      const int32_t* enable, v2d_stream_t stream);
+
+/* counts[b] = {|S_kf|, |S_curr ∩ S_kf|} = {#kf_member, #(kf_member and alive)}. */
+int v2d_track_survival(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                       int32_t* counts, v2d_stream_t stream);
+
+/* Rig-wide Eq. 5 over n images' counts: *flag = 1 iff sum|S_kf| == 0 (bootstrap)
+ * or sum|S_curr ∩ S_kf| < T * sum|S_kf| (fp64), else 0.  totals (nullable,
+ * int64[2]) receives the sums.  Multi-GPU: all-reduce the counts first. */
+int v2d_keyframe_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
+                        v2d_stream_t stream);
+
+/* If *flag: the j-th valid detection of image b (cell-major slot order of
+ * v2d_detect_gftt's kp_xy, the first cell_count slots of each cell) fills the
+ * j-th dead slot (ascending): status := V2D_TRACKED, id := next_id + j; then
+ * kf_member := alive for every slot and next_id advances.  No-op if *flag == 0.
+ * grid_x*grid_y <= 1024. */
+int v2d_refill_tracks(const float* kp_xy, const int32_t* cell_count, int grid_x, int grid_y,
+                      int k, const int32_t* flag, int B, int P, float* tracks, uint8_t* status,
+                      uint8_t* kf_member, int32_t* track_id, int32_t* next_id,
+                      v2d_stream_t stream);
 
 /* Static string for a V2D_* return code. */
 const char* v2d_strerror(int code);

@@ -58,11 +58,14 @@ def lib() -> ctypes.CDLL:
         L.v2dref_lambda_min.restype = d
         L.v2dref_response.argtypes = [P, i64, i, i, P, P]
         L.v2dref_grid_k.argtypes = [i, i, i, i, P]
-        L.v2dref_detect_gftt.argtypes = [P, i64, i, i, i, i, i, i, f, i, i, P, P, P]
+        L.v2dref_detect_gftt.argtypes = [P, i64, i, i, i, i, i, i, f, i, i, P, P, P, P]
         L.v2dref_ncc.argtypes = [P, P, i]
         L.v2dref_ncc.restype = d
         L.v2dref_track_klt.argtypes = [P, P, i, i, i, P, P, P, i, i, i, d, d, d, i, P, P, P, P]
         L.v2dref_extract_patches.argtypes = [P, i, i, i, P, i, i, P]
+        L.v2dref_suppress_mask.argtypes = [P, P, i, d, i, i, P]
+        L.v2dref_keyframe_due.argtypes = [i64, i64, d]
+        L.v2dref_refill.argtypes = [P, P, i, i, i, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -142,7 +145,8 @@ def grid_k(grid_x: int, grid_y: int, k: int, K_min: int) -> int:
 
 
 def detect_gftt(img: np.ndarray, grid_x: int, grid_y: int, k: int = 0, K_min: int = 0,
-                min_score: float = 0.0, border: int = 3, nms: int = 1):
+                min_score: float = 0.0, border: int = 3, nms: int = 1,
+                mask: np.ndarray | None = None):
     """D5-D6: (kp_xy float32 [gy,gx,k,2], kp_score float32 [gy,gx,k], count int32 [gy*gx])."""
     img = np.ascontiguousarray(img, dtype=np.uint8)
     H, W = img.shape
@@ -150,8 +154,12 @@ def detect_gftt(img: np.ndarray, grid_x: int, grid_y: int, k: int = 0, K_min: in
     xy = np.zeros((grid_y, grid_x, kk, 2), np.float32)
     sc = np.zeros((grid_y, grid_x, kk), np.float32)
     cnt = np.zeros(grid_y * grid_x, np.int32)
+    if mask is not None:
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        assert mask.shape == img.shape
     _check(lib().v2dref_detect_gftt(_ptr(img), img.strides[0], W, H, grid_x, grid_y, k, K_min,
-                                    float(min_score), border, nms, _ptr(xy), _ptr(sc), _ptr(cnt)),
+                                    float(min_score), border, nms, _ptr(mask), _ptr(xy), _ptr(sc),
+                                    _ptr(cnt)),
            "detect_gftt")
     return xy, sc, cnt
 
@@ -194,3 +202,30 @@ def extract_patches(dense_pyr: np.ndarray, W: int, H: int, levels: int, pts: np.
     _check(lib().v2dref_extract_patches(_ptr(dense_pyr), W, H, levels, _ptr(pts), pts.shape[0],
                                         patch, _ptr(out)), "extract_patches")
     return out
+
+
+# ---- variant f1 ------------------------------------------------------------
+def suppress_mask(tracks: np.ndarray, status: np.ndarray, min_sep: float, W: int, H: int):
+    """status: KLT status per track (0 = alive)."""
+    tracks = np.ascontiguousarray(tracks, np.float32).reshape(-1, 2)
+    status = np.ascontiguousarray(status, np.uint8).ravel()
+    mask = np.zeros((H, W), np.uint8)
+    _check(lib().v2dref_suppress_mask(_ptr(tracks), _ptr(status), tracks.shape[0],
+                                      float(min_sep), W, H, _ptr(mask)), "suppress_mask")
+    return mask
+
+
+def keyframe_due(n_kf: int, n_surv: int, T: float) -> bool:
+    return bool(lib().v2dref_keyframe_due(int(n_kf), int(n_surv), float(T)))
+
+
+def refill(kp_xy, cell_count, k, tracks, status, kf_member, track_id, next_id: int):
+    """In place on numpy arrays (tracks f32 [P,2], status/kf_member u8 [P],
+    track_id i32 [P]); returns the new next_id."""
+    kp_xy = np.ascontiguousarray(kp_xy, np.float32)
+    cell_count = np.ascontiguousarray(cell_count, np.int32).ravel()
+    nid = np.array([next_id], np.int32)
+    _check(lib().v2dref_refill(_ptr(kp_xy), _ptr(cell_count), cell_count.size, k,
+                               status.size, _ptr(tracks), _ptr(status), _ptr(kf_member),
+                               _ptr(track_id), _ptr(nid)), "refill")
+    return int(nid[0])

@@ -220,7 +220,7 @@ static int cmp_key_desc(const void* pa, const void* pb) {
 
 int v2dref_detect_gftt(const uint8_t* img, int64_t pitch, int W, int H,
                        int grid_x, int grid_y, int k, int K_min,
-                       float min_score, int border, int nms,
+                       float min_score, int border, int nms, const uint8_t* mask,
                        float* kp_xy, float* kp_score, int32_t* cell_count) {
   int kk;
   if (!img || !kp_xy || !kp_score || !cell_count || pitch < W) return V2DREF_EINVAL;
@@ -249,6 +249,7 @@ int v2dref_detect_gftt(const uint8_t* img, int64_t pitch, int W, int H,
           /* D5 eligibility */
           if (x < border || x > W - 1 - border || y < border || y > H - 1 - border) continue;
           if (!(R[(int64_t)y * W + x] > min_score)) continue;
+          if (mask && mask[(int64_t)y * pitch + x]) continue; /* f1 min_separation */
           uint64_t kp = key_of(R, W, x, y);
           int is_max = 1;
           if (nms) /* strict 3x3 local maximum by key (reading #5) */
@@ -514,5 +515,58 @@ int v2dref_extract_patches(const double* pyr, int W, int H, int levels, const fl
       off += (int64_t)Ws[L] * Hs[L];
     }
   }
+  return V2DREF_OK;
+}
+
+/* ------------------------------------------------------- f1 keyframes -- */
+/* "keypoints closer than min_separation to an existing live track are
+ * suppressed". */
+int v2dref_suppress_mask(const float* tracks, const uint8_t* status, int P, double min_sep,
+                         int W, int H, uint8_t* mask) {
+  if (!mask || W < 1 || H < 1 || P < 0 || !(min_sep >= 0.0)) return V2DREF_EINVAL;
+  for (int64_t i = 0; i < (int64_t)W * H; ++i) mask[i] = 0;
+  for (int p = 0; p < P; ++p) {
+    if (status[p] != V2DREF_TRACKED) continue;
+    double tx = tracks[2 * p], ty = tracks[2 * p + 1];
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        double dx = x - tx, dy = y - ty;
+        if (dx * dx + dy * dy < min_sep * min_sep) mask[(int64_t)y * W + x] = 1;
+      }
+  }
+  return V2DREF_OK;
+}
+
+/* Eq. 5: a keyframe is created if |S_curr ∩ S_kf| / |S_kf| < T. */
+int v2dref_keyframe_due(int64_t n_kf, int64_t n_surv, double T) {
+  if (n_kf == 0) return 1; /* bootstrap: the first frame is a keyframe */
+  return ((double)n_surv / (double)n_kf) < T ? 1 : 0;
+}
+
+int v2dref_refill(const float* kp_xy, const int32_t* cell_count, int cells, int k, int P,
+                  float* tracks, uint8_t* status, uint8_t* kf_member, int32_t* track_id,
+                  int32_t* next_id) {
+  if (!kp_xy || !cell_count || !tracks || !status || !kf_member || !track_id || !next_id)
+    return V2DREF_EINVAL;
+  /* valid detections in slot order */
+  int n_new = 0;
+  for (int c = 0; c < cells; ++c) n_new += cell_count[c];
+  int j = 0, c = 0, r = 0;
+  for (int p = 0; p < P && j < n_new; ++p) {
+    if (status[p] == V2DREF_TRACKED) continue;
+    while (r >= cell_count[c]) {
+      ++c;
+      r = 0;
+    }
+    int64_t src = (int64_t)c * k + r;
+    tracks[2 * p] = kp_xy[2 * src];
+    tracks[2 * p + 1] = kp_xy[2 * src + 1];
+    status[p] = V2DREF_TRACKED;
+    track_id[p] = *next_id + j;
+    ++j;
+    ++r;
+  }
+  *next_id += j;
+  for (int p = 0; p < P; ++p) kf_member[p] = status[p] == V2DREF_TRACKED;
   return V2DREF_OK;
 }

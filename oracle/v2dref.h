@@ -72,10 +72,12 @@ int v2dref_grid_k(int grid_x, int grid_y, int k, int K_min, int* k_out);
 /* D5-D6: eligibility, 3x3 NMS on the 64-bit key, per-cell top-k.
  * kp_xy [gy][gx][k][2], kp_score [gy][gx][k], cell_count [gy*gx]; k is the
  * value v2dref_grid_k resolves.  Unfilled slots: (-1,-1), score 0.
+ * mask (nullable, row pitch = pitch): non-zero pixels are not eligible
+ * (min_separation suppression; variant f1).
  * EINVAL: border < 3, grid cell < 1 px, bad k, W or H < 2*border+1. */
 int v2dref_detect_gftt(const uint8_t* img, int64_t pitch, int W, int H,
                        int grid_x, int grid_y, int k, int K_min,
-                       float min_score, int border, int nms,
+                       float min_score, int border, int nms, const uint8_t* mask,
                        float* kp_xy, float* kp_score, int32_t* cell_count);
 
 /* Two-pass NCC of two n-vectors; 0 if the denominator is 0 (reading #14). */
@@ -111,6 +113,20 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
  * empty slots (-1,-1) give zeros.  pyr: dense pyramid of v2dref_build_pyramid. */
 int v2dref_extract_patches(const double* pyr, int W, int H, int levels, const float* pts, int P,
                            int patch, double* out);
+
+/* ---- variant f1 (Eq. 5) ---- */
+/* Track tables use the KLT status as liveness: status 0 (TRACKED) = alive.
+ * mask[y*W + x] = 1 iff (x-tx)^2 + (y-ty)^2 < min_sep^2 for an alive track. */
+int v2dref_suppress_mask(const float* tracks, const uint8_t* status, int P, double min_sep,
+                         int W, int H, uint8_t* mask);
+/* SPEC keyframe_due: 1 iff n_surv / n_kf < T (bootstrap: n_kf == 0 -> 1). */
+int v2dref_keyframe_due(int64_t n_kf, int64_t n_surv, double T);
+/* Refill dead slots (status != 0, ascending) with the valid detections in slot
+ * order (first cell_count[c] slots of each cell c): status := 0, ids next_id + j;
+ * then kf_member := (status == 0). */
+int v2dref_refill(const float* kp_xy, const int32_t* cell_count, int cells, int k, int P,
+                  float* tracks, uint8_t* status, uint8_t* kf_member, int32_t* track_id,
+                  int32_t* next_id);
 
 #ifdef __cplusplus
 }

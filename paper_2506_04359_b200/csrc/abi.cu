@@ -87,6 +87,7 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
 int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
                     int grid_x, int grid_y, int k, int K_min, float min_score, int border,
                     int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
+                    const uint8_t* const* mask_ptrs, const int32_t* enable,
                     v2d_stream_t stream) {
   int kk = 0;
   if (B < 0 || B > 65535) return V2D_EINVAL;
@@ -101,7 +102,7 @@ int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int 
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
   if (l0_pitch * (int64_t)H >= ((int64_t)1 << 31)) return V2D_EINVAL;  // 32-bit row offsets
   v2d::GfttArgs a{W, H, grid_x, grid_y, kk, border, nms, min_score, l0_pitch};
-  return v2d::launch_gftt(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp,
+  return v2d::launch_gftt(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp, mask_ptrs, enable,
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -139,6 +140,43 @@ int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_p
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
   return v2d::launch_patches(l0_ptrs, pyr_ptrs, l0_pitch, B, lv, pts, P, patch, out,
                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_suppress_mask(const float* tracks, const uint8_t* status, int B, int P, float min_sep,
+                      int W, int H, uint8_t* const* mask_ptrs, int64_t mask_pitch,
+                      const int32_t* enable, v2d_stream_t stream) {
+  if (B < 0 || B > 65535 || P < 0 || W < 1 || H < 1 || !(min_sep >= 0.0f)) return V2D_EINVAL;
+  if (B > 0 && (!mask_ptrs || (P > 0 && (!tracks || !status)))) return V2D_EINVAL;
+  if (mask_pitch < W || (mask_pitch % 16) != 0) return V2D_EALIGN;
+  return v2d::launch_suppress(mask_ptrs, mask_pitch, B, W, H, tracks, status, P, min_sep, enable,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_track_survival(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                       int32_t* counts, v2d_stream_t stream) {
+  if (B < 0 || P < 0 || (B > 0 && (!counts || (P > 0 && (!status || !kf_member)))))
+    return V2D_EINVAL;
+  return v2d::launch_survival(status, kf_member, B, P, counts,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_keyframe_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
+                        v2d_stream_t stream) {
+  if (n < 0 || !flag || (n > 0 && !counts) || !(T >= 0.0f)) return V2D_EINVAL;
+  return v2d::launch_decide(counts, n, T, flag, totals, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_refill_tracks(const float* kp_xy, const int32_t* cell_count, int grid_x, int grid_y,
+                      int k, const int32_t* flag, int B, int P, float* tracks, uint8_t* status,
+                      uint8_t* kf_member, int32_t* track_id, int32_t* next_id,
+                      v2d_stream_t stream) {
+  if (B < 0 || P < 0 || grid_x < 1 || grid_y < 1 || grid_x * grid_y > 1024 || k < 1 || !flag)
+    return V2D_EINVAL;
+  if (B > 0 && (!kp_xy || !cell_count || !tracks || !status || !kf_member || !track_id ||
+                !next_id))
+    return V2D_EINVAL;
+  return v2d::launch_refill(kp_xy, cell_count, grid_x * grid_y, k, flag, B, P, tracks, status,
+                            kf_member, track_id, next_id, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

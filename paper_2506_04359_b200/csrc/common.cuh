@@ -31,7 +31,8 @@ struct GfttArgs {
   int64_t pitch;
 };
 int launch_gftt(const uint8_t* const* l0_ptrs, int B, const GfttArgs& a, float* kp_xy,
-                float* kp_score, int32_t* cell_count, float* resp, cudaStream_t st);
+                float* kp_score, int32_t* cell_count, float* resp,
+                const uint8_t* const* mask_ptrs, const int32_t* enable, cudaStream_t st);
 
 struct KltArgs {
   int W, H, P, win, iters;
@@ -48,5 +49,16 @@ int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
 int launch_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs, int64_t l0_pitch,
                    int B, const Levels& lv, const float* pts, int P, int patch, float* out,
                    cudaStream_t st);
+
+int launch_suppress(uint8_t* const* mask_ptrs, int64_t pitch, int B, int W, int H,
+                    const float* tracks, const uint8_t* status, int P, float min_sep,
+                    const int32_t* enable, cudaStream_t st);
+int launch_survival(const uint8_t* status, const uint8_t* kf_member, int B, int P, int32_t* counts,
+                    cudaStream_t st);
+int launch_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
+                  cudaStream_t st);
+int launch_refill(const float* kp_xy, const int32_t* cell_count, int cells, int k,
+                  const int32_t* flag, int B, int P, float* tracks, uint8_t* status,
+                  uint8_t* kf_member, int32_t* track_id, int32_t* next_id, cudaStream_t st);
 
 }  // namespace v2d

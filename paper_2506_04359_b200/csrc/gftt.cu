@@ -95,7 +95,10 @@ __device__ __forceinline__ int lazy_int_threshold(float s) {
 __global__ void __launch_bounds__(kThreads)
 gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
                  float* __restrict__ kp_xy, float* __restrict__ kp_score,
-                 int32_t* __restrict__ cell_count, float* __restrict__ resp) {
+                 int32_t* __restrict__ cell_count, float* __restrict__ resp,
+                 const uint8_t* const* __restrict__ mask_ptrs,
+                 const int32_t* __restrict__ enable) {
+  if (enable && enable[0] == 0) return;  // keyframe-conditional detection (f1)
   __shared__ unsigned long long s_buf[kWarps * kWBuf];
   __shared__ __align__(16) float s_ring[kWarps][3][kRing];
   __shared__ int s_cnt[kWarps][2];  // [0] = kept (top), [1] = fresh candidates
@@ -107,6 +110,7 @@ gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
   const int cell = blockIdx.x, b = blockIdx.y;
   const int cx = cell % a.grid_x, cy = cell / a.grid_x;
   const uint8_t* __restrict__ img = l0_ptrs[b];
+  const uint8_t* __restrict__ mask = mask_ptrs ? mask_ptrs[b] : nullptr;
   const int64_t pitch = a.pitch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -277,6 +281,7 @@ gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
           if (a.nms)
             ok = ok && rp > u[j] && rp > u[j + 1] && rp > u[j + 2] && rp > m[j] &&
                  rp >= m[j + 2] && rp >= d[j] && rp >= d[j + 1] && rp >= d[j + 2];
+          if (ok && mask) ok = mask[(int64_t)yn * pitch + x] == 0;  // min_separation (f1)
           if (ok) {
             const unsigned long long kp = make_key(rp, x, yn, W);
             if (kp > thr) {
@@ -369,10 +374,12 @@ gftt_topk_kernel(const uint8_t* const* __restrict__ l0_ptrs, GfttArgs a,
 }  // namespace
 
 int launch_gftt(const uint8_t* const* l0_ptrs, int B, const GfttArgs& a, float* kp_xy,
-                float* kp_score, int32_t* cell_count, float* resp, cudaStream_t st) {
+                float* kp_score, int32_t* cell_count, float* resp,
+                const uint8_t* const* mask_ptrs, const int32_t* enable, cudaStream_t st) {
   if (B == 0) return V2D_OK;
   dim3 grid(a.grid_x * a.grid_y, B);
-  gftt_topk_kernel<<<grid, kThreads, 0, st>>>(l0_ptrs, a, kp_xy, kp_score, cell_count, resp);
+  gftt_topk_kernel<<<grid, kThreads, 0, st>>>(l0_ptrs, a, kp_xy, kp_score, cell_count, resp,
+                                              mask_ptrs, enable);
   return cudaGetLastError() == cudaSuccess ? V2D_OK : V2D_ECUDA;
 }
 

@@ -124,3 +124,96 @@ class RingSchedule:
     def tables(self, step: int):
         i = step % self.n_steps
         return self.cur[i], self.prev[i], i % 2
+
+
+class KeyframeTracker:
+    """Variant f1: keyframe-driven continuous tracking of one
+    rig, one frame per step (B = C cameras).  Per frame:
+
+        v2d_build_pyramid   (frame t)
+        v2d_track_klt       (live tracks t-1 -> t; lost slots are SKIPPED because the
+                             status table is fed back as in_status: lost is terminal)
+        v2d_track_survival  (per camera |S_kf|, |S_curr ∩ S_kf|)
+        v2d_keyframe_decide (rig-wide Eq. 5 into a device flag; multi-GPU: the totals
+                             are all-reduced first)
+        -- device-flag gated, no host round trip --
+        v2d_suppress_mask   (min_separation disks around live tracks)
+        v2d_detect_gftt     (masked grid top-k)
+        v2d_refill_tracks   (new tracks into dead slots, new ids; S_kf := alive)
+
+    The track table is double-buffered: KLT reads table i and writes table 1-i.
+    """
+
+    def __init__(self, cfg: FrontendConfig, cams: int, device, l0_pitch: int, T: float = 0.7,
+                 min_sep: float | None = None, group=None):
+        self.cfg, self.C, self.dev, self.pitch = cfg, cams, torch.device(device), l0_pitch
+        self.T = T
+        self.min_sep = float(cfg.win // 2 if min_sep is None else min_sep)
+        self.group = group
+        self.layout = v2d.pyramid_layout(cfg.W, cfg.H, cfg.levels)
+        self.k = v2d.grid_k(cfg.grid_x, cfg.grid_y, cfg.k, cfg.K_min)
+        self.P = cfg.grid_x * cfg.grid_y * self.k
+        C, P, d = cams, self.P, self.dev
+        n = max(int(self.layout.floats_per_image), 32)
+        self.pyr = torch.zeros((2, C, n), dtype=torch.float32, device=d)
+        self.pyr_ptrs = [v2d.ptrs_of(self.pyr[i]) for i in range(2)]
+        self.tracks = torch.full((2, C, P, 2), -1.0, dtype=torch.float32, device=d)
+        self.status = torch.full((2, C, P), v2d.SKIPPED, dtype=torch.uint8, device=d)
+        self.kf_member = torch.zeros((C, P), dtype=torch.uint8, device=d)
+        self.track_id = torch.full((C, P), -1, dtype=torch.int32, device=d)
+        self.next_id = torch.zeros((C,), dtype=torch.int32, device=d)
+        self.mask = torch.zeros((C, cfg.H, l0_pitch), dtype=torch.uint8, device=d)
+        self.mask_ptrs = v2d.ptrs_of(self.mask)
+        self.kp_xy = torch.full((C, cfg.grid_y, cfg.grid_x, self.k, 2), -1.0, device=d)
+        self.kp_score = torch.zeros((C, cfg.grid_y, cfg.grid_x, self.k), device=d)
+        self.cell_count = torch.zeros((C, cfg.grid_x * cfg.grid_y), dtype=torch.int32, device=d)
+        self.counts = torch.zeros((C, 2), dtype=torch.int32, device=d)
+        self.flag = torch.zeros((1,), dtype=torch.int32, device=d)
+        self.totals = torch.zeros((2,), dtype=torch.int64, device=d)
+        self.ncc = torch.zeros((C, P), device=d)
+        self.iters = torch.zeros((C, P), dtype=torch.int32, device=d)
+        self.cur = 0
+
+    def _keyframe_branch(self, l0_ptrs, j):
+        c, C, P = self.cfg, self.C, self.P
+        v2d.suppress_mask_ptrs(self.tracks[j], self.status[j], C, P, self.min_sep, c.W, c.H,
+                               self.mask_ptrs, self.pitch, self.flag)
+        v2d.detect_gftt_ptrs(l0_ptrs, self.pitch, C, c.W, c.H, c.grid_x, c.grid_y, c.k, c.K_min,
+                             c.min_score, c.border, c.nms, self.kp_xy, self.kp_score,
+                             self.cell_count, None, self.mask_ptrs, self.flag)
+        v2d.refill_tracks(self.kp_xy, self.cell_count, c.grid_x, c.grid_y, self.k, self.flag,
+                          self.tracks[j], self.status[j], self.kf_member, self.track_id,
+                          self.next_id)
+
+    def start(self, l0_ptrs: torch.Tensor):
+        """First frame: pyramid + bootstrap keyframe (Eq. 5 with empty S_kf)."""
+        c = self.cfg
+        v2d.build_pyramid_ptrs(l0_ptrs, self.pitch, self.C, c.W, c.H, c.levels,
+                               self.pyr_ptrs[self.cur])
+        self.flag.fill_(1)
+        self._keyframe_branch(l0_ptrs, self.cur)
+
+    def step(self, l0_ptrs: torch.Tensor, prev_l0_ptrs: torch.Tensor):
+        c, C, P = self.cfg, self.C, self.P
+        i, j = self.cur, 1 - self.cur
+        v2d.build_pyramid_ptrs(l0_ptrs, self.pitch, C, c.W, c.H, c.levels, self.pyr_ptrs[j])
+        v2d.track_klt_ptrs(prev_l0_ptrs, self.pyr_ptrs[i], l0_ptrs, self.pyr_ptrs[j], self.pitch,
+                           C, c.W, c.H, c.levels, self.tracks[i], None, self.status[i], P, c.win,
+                           c.iters, c.eps, c.ncc_min, c.min_eig, self.tracks[j], self.status[j],
+                           self.ncc, self.iters, c.klt_flags)
+        v2d.track_survival(self.status[j], self.kf_member, self.counts)
+        if self.group is not None:
+            import torch.distributed as dist
+            v2d.keyframe_decide(self.counts, self.T, self.flag, self.totals)
+            dist.all_reduce(self.totals, group=self.group)  # rig-wide Eq. 5 (NCCL)
+            red = self.totals.to(torch.int32).view(1, 2)
+            v2d.keyframe_decide(red, self.T, self.flag)
+        else:
+            v2d.keyframe_decide(self.counts, self.T, self.flag, self.totals)
+        self._keyframe_branch(l0_ptrs, j)
+        self.cur = j
+
+    def table(self):
+        """(tracks [C,P,2], status [C,P], kf_member, track_id, next_id) of the current frame."""
+        return (self.tracks[self.cur], self.status[self.cur], self.kf_member, self.track_id,
+                self.next_id)

@@ -36,7 +36,8 @@ class Layout(ctypes.Structure):
 
 
 _SYMBOLS = ("v2d_pyramid_layout", "v2d_grid_k", "v2d_build_pyramid", "v2d_detect_gftt",
-            "v2d_track_klt", "v2d_extract_patches", "v2d_strerror", "v2d_version")
+            "v2d_track_klt", "v2d_extract_patches", "v2d_suppress_mask", "v2d_track_survival",
+            "v2d_keyframe_decide", "v2d_refill_tracks", "v2d_strerror", "v2d_version")
 
 _lib = None
 
@@ -54,7 +55,12 @@ def load() -> ctypes.CDLL:
     L.v2d_pyramid_layout.argtypes = [i, i, i, ctypes.POINTER(Layout)]
     L.v2d_grid_k.argtypes = [i, i, i, i, ctypes.POINTER(ctypes.c_int)]
     L.v2d_build_pyramid.argtypes = [vp, i64, i, i, i, i, vp, vp]
-    L.v2d_detect_gftt.argtypes = [vp, i64, i, i, i, i, i, i, i, f, i, i, vp, vp, vp, vp, vp]
+    L.v2d_detect_gftt.argtypes = [vp, i64, i, i, i, i, i, i, i, f, i, i, vp, vp, vp, vp, vp, vp,
+                                  vp]
+    L.v2d_suppress_mask.argtypes = [vp, vp, i, i, f, i, i, vp, i64, vp, vp]
+    L.v2d_track_survival.argtypes = [vp, vp, i, i, vp, vp]
+    L.v2d_keyframe_decide.argtypes = [vp, i, f, vp, vp, vp]
+    L.v2d_refill_tracks.argtypes = [vp, vp, i, i, i, vp, i, i, vp, vp, vp, vp, vp, vp]
     L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
                                 vp, vp, vp, vp, ctypes.c_uint, vp]
     L.v2d_extract_patches.argtypes = [vp, vp, i64, i, i, i, i, vp, i, i, vp, vp]
@@ -127,11 +133,12 @@ def build_pyramid_ptrs(l0_ptrs, l0_pitch, B, W, H, levels, pyr_ptrs):
 
 
 def detect_gftt_ptrs(l0_ptrs, l0_pitch, B, W, H, grid_x, grid_y, k, K_min, min_score, border,
-                     nms, kp_xy, kp_score, cell_count, resp=None):
-    _need_cuda(kp_xy, kp_score, cell_count, resp)
+                     nms, kp_xy, kp_score, cell_count, resp=None, mask_ptrs=None, enable=None):
+    _need_cuda(kp_xy, kp_score, cell_count, resp, enable)
     _check(load().v2d_detect_gftt(_p(l0_ptrs), l0_pitch, B, W, H, grid_x, grid_y, k, K_min,
                                   float(min_score), border, nms, _p(kp_xy), _p(kp_score),
-                                  _p(cell_count), _p(resp), _stream()), "detect_gftt")
+                                  _p(cell_count), _p(resp), _p(mask_ptrs), _p(enable),
+                                  _stream()), "detect_gftt")
 
 
 def track_klt_ptrs(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, l0_pitch, B, W, H,
@@ -169,7 +176,7 @@ def build_pyramid(frames: torch.Tensor, W: int, levels: int, out: torch.Tensor |
 
 def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int = 0,
                 K_min: int = 0, min_score: float = 0.0, border: int = 11, nms: int = 1,
-                want_resp: bool = False):
+                want_resp: bool = False, mask: torch.Tensor | None = None):
     """-> (kp_xy [B,gy,gx,k,2], kp_score [B,gy,gx,k], cell_count [B,gy*gx], resp|None)."""
     B, H, pitch = _frames(frames)
     kk = grid_k(grid_x, grid_y, k, K_min)
@@ -178,8 +185,10 @@ def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int =
     sc = torch.empty((B, grid_y, grid_x, kk), dtype=torch.float32, device=dev)
     cnt = torch.empty((B, grid_y * grid_x), dtype=torch.int32, device=dev)
     resp = torch.empty((B, H, W), dtype=torch.float32, device=dev) if want_resp else None
+    if mask is not None and (mask.shape != frames.shape or mask.dtype != torch.uint8):
+        raise V2DError("mask must be uint8 with the frames' shape [B, H, pitch]")
     detect_gftt_ptrs(ptrs_of(frames), pitch, B, W, H, grid_x, grid_y, k, K_min, min_score,
-                     border, nms, xy, sc, cnt, resp)
+                     border, nms, xy, sc, cnt, resp, None if mask is None else ptrs_of(mask))
     return xy, sc, cnt, resp
 
 
@@ -249,3 +258,35 @@ def cross_camera_track(src_frames, src_pyr, dst_frames, dst_pyr, W: int, levels:
     guess = torch.tensor(disparity_prior, dtype=torch.float32, device=pts.device)
     guess = guess.view(1, 1, 2).expand(B, P, 2).contiguous()
     return track_klt(src_frames, src_pyr, dst_frames, dst_pyr, W, levels, pts, guess=guess, **kw)
+
+
+# --------------------------------------------------------------------------
+# variant f1: keyframe-driven continuous tracking
+# --------------------------------------------------------------------------
+def suppress_mask_ptrs(tracks, status, B, P, min_sep, W, H, mask_ptrs, mask_pitch, enable=None):
+    _need_cuda(tracks, status, enable)
+    _check(load().v2d_suppress_mask(_p(tracks), _p(status), B, P, float(min_sep), W, H,
+                                    _p(mask_ptrs), mask_pitch, _p(enable), _stream()),
+           "suppress_mask")
+
+
+def track_survival(status, kf_member, counts):
+    B, P = status.shape
+    _need_cuda(status, kf_member, counts)
+    _check(load().v2d_track_survival(_p(status), _p(kf_member), B, P, _p(counts), _stream()),
+           "track_survival")
+
+
+def keyframe_decide(counts, T, flag, totals=None):
+    _need_cuda(counts, flag, totals)
+    _check(load().v2d_keyframe_decide(_p(counts), counts.shape[0], float(T), _p(flag),
+                                      _p(totals), _stream()), "keyframe_decide")
+
+
+def refill_tracks(kp_xy, cell_count, grid_x, grid_y, k, flag, tracks, status, kf_member,
+                  track_id, next_id):
+    B, P = status.shape
+    _need_cuda(kp_xy, cell_count, flag, tracks, status, kf_member, track_id, next_id)
+    _check(load().v2d_refill_tracks(_p(kp_xy), _p(cell_count), grid_x, grid_y, k, _p(flag), B, P,
+                                    _p(tracks), _p(status), _p(kf_member), _p(track_id),
+                                    _p(next_id), _stream()), "refill_tracks")

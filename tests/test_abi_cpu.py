@@ -80,10 +80,10 @@ def test_validation_without_gpu(v2d):
     assert L.v2d_build_pyramid(N, 64, 0, 64, 64, 9, N, N) == -1
     assert L.v2d_build_pyramid(N, 40, 0, 33, 10, 2, N, N) == -2
     # detect: border < 3, Eq. 1 violation, nms not 0/1, grid cell < 1 px
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 2, 1, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 256, 0.0, 3, 1, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 3, 2, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 65, 8, 4, 0, 0.0, 3, 1, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 2, 1, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 256, 0.0, 3, 1, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 3, 2, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 65, 8, 4, 0, 0.0, 3, 1, N, N, N, N, N, N, N) == -1
     # klt: even window, window too large, iters < 1, bad pitch
     args = dict(eps=0.01, ncc=0.8, eig=0.01)
     f = ctypes.c_float
@@ -125,3 +125,14 @@ def test_binding_requires_cuda_tensors(v2d):
     import torch
     with pytest.raises((v2d.V2DError, RuntimeError, AssertionError)):
         v2d.build_pyramid(torch.zeros((1, 16, 16), dtype=torch.uint8), 16, 2)
+
+
+def test_keyframe_calls_validate_without_gpu(v2d):
+    L = v2d.load()
+    N = None
+    f = ctypes.c_float
+    assert L.v2d_suppress_mask(N, N, 1, 4, f(5.0), 64, 64, N, 64, N, N) == -1   # null mask ptrs
+    assert L.v2d_suppress_mask(N, N, 0, 0, f(5.0), 64, 64, N, 40, N, N) == -2   # pitch % 16
+    assert L.v2d_keyframe_decide(N, 0, f(0.7), N, N, N) == -1                   # null flag
+    assert L.v2d_refill_tracks(N, N, 64, 32, 4, N, 0, 0, N, N, N, N, N, N) == -1  # > 1024 cells
+    assert L.v2d_extract_patches(N, N, 64, 0, 64, 64, 2, N, 0, 8, N, N) == -1   # even patch

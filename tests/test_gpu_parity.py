@@ -253,3 +253,59 @@ def test_cross_camera_parity():
     a = v2d.cross_camera_track(dl, pl, dr, pr, W, 3, tp, disparity_prior=(-17.5, 0.5))
     b = v2d.track_klt(dl, pl, dr, pr, W, 3, tp, guess=torch.from_numpy(guess).cuda())
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ------------------------------------------------------------ f1 keyframes
+def test_keyframe_tracker_stepwise_parity():
+    """Variant f1, per frame: the KLT part vs the oracle on the GPU's previous
+    table (bands), then the rig-wide Eq. 5 decision, suppression, masked
+    detection and refill vs the oracle on the GPU's own KLT output (exact)."""
+    from paper_2506_04359_b200.frontend import KeyframeTracker
+    W, H, C, levels = 320, 240, 2, 3
+    wl = synth.Workload("kf", 12, W, H, C, levels, grid_x=4, grid_y=3, k=6, motion=(7.0, 5.0),
+                        stereo_disparity=0.0)
+    st = synth.make_stream(wl, 7, "cpu")
+    frames = st.frames[:, :, :, :W].numpy().copy()         # [C, T, H, W]
+    dev = st.frames.cuda()                                  # [C, T, H, pitch]
+    cfg = v2d.FrontendConfig(W=W, H=H, levels=levels, grid_x=4, grid_y=3, k=6, border=11)
+    T, ms = 0.9, 8.0
+    kt = KeyframeTracker(cfg, C, "cuda", wl.pitch, T=T, min_sep=ms)
+    ptr = lambda t: v2d.ptrs_of(dev[:, t])
+    kt.start(ptr(0))
+    n_kf_frames = 0
+    for t in range(1, 7):
+        tr0, st0, kf0, id0, nid0 = [x.clone().cpu().numpy() for x in kt.table()]
+        kt.step(ptr(t), ptr(t - 1))
+        tr1, st1, kf1, id1, nid1 = [x.cpu().numpy() for x in kt.table()]
+        flag = int(kt.flag.item())
+        refilled = (id1 != id0)
+        counts_kf, counts_sv = 0, 0
+        pre_tracks, pre_status = tr1.copy(), st1.copy()
+        for c in range(C):
+            pre_status[c][refilled[c]] = 4
+            pre_tracks[c][refilled[c]] = -1
+            # KLT part vs oracle (oracle fed the GPU's previous table)
+            _, dp = oracle.build_pyramid(frames[c, t - 1], levels)
+            _, dc = oracle.build_pyramid(frames[c, t], levels)
+            opos, ost, onc, dg = oracle.track_klt(dp, dc, W, H, levels, tr0[c], in_status=st0[c])
+            keep = ~refilled[c]
+            compare_klt(tr0[c][keep], pre_tracks[c][keep], pre_status[c][keep], opos[keep],
+                        ost[keep], dg[keep])
+            counts_kf += int(kf0[c].sum())
+            counts_sv += int((kf0[c].astype(bool) & (pre_status[c] == 0)).sum())
+        assert flag == int(oracle.keyframe_due(counts_kf, counts_sv, T))
+        n_kf_frames += flag
+        for c in range(C):
+            otr, ost_, okf, oid = pre_tracks[c].copy(), pre_status[c].copy(), kf0[c].copy(), id0[c].copy()
+            onid = int(nid0[c])
+            if flag:
+                mask = oracle.suppress_mask(otr, ost_, ms, W, H)
+                gmask = kt.mask[c, :, :W].cpu().numpy()
+                assert np.array_equal(gmask, mask)
+                xy, sc, cnt = oracle.detect_gftt(frames[c, t], 4, 3, k=6, border=11, mask=mask)
+                assert np.array_equal(kt.kp_xy[c].cpu().numpy(), xy)
+                onid = oracle.refill(xy.reshape(-1, 2), cnt, 6, otr, ost_, okf, oid, onid)
+            assert np.array_equal(st1[c], ost_) and np.array_equal(id1[c], oid)
+            assert np.array_equal(kf1[c], okf) and int(nid1[c]) == onid
+            assert np.array_equal(tr1[c][refilled[c]], otr[refilled[c]])
+    assert n_kf_frames >= 1
