@@ -100,6 +100,10 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
  *   cell_count [B][grid_y*grid_x]        int32 filled slots per cell
  *   resp       nullable [B][H][W] fp32: full R map (0 outside 2..W-3 x 2..H-3);
  *              when given, the lazy-eigenvalue shortcut is disabled.
+ *   workspace  nullable [B][H][round_up(W,32)] fp32 scratch (16-B aligned).  When
+ *              given, K2 runs as two dense
+ *              passes (per-pixel candidate map, then per-cell selection); when
+ *              NULL, as one fused per-cell kernel.  Results are identical.
  *   mask_ptrs  nullable device array [B] of u8 masks (row pitch l0_pitch); a
  *              non-zero mask pixel is not eligible (min_separation suppression,
  *              S:158; NMS still compares against it)
@@ -110,7 +114,7 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
 int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
                     int grid_x, int grid_y, int k, int K_min, float min_score, int border,
                     int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
-                    const uint8_t* const* mask_ptrs, const int32_t* enable,
+                    float* workspace, const uint8_t* const* mask_ptrs, const int32_t* enable,
                     v2d_stream_t stream);
 
 /* Pyramidal LK tracking (LK_1981, LK_2000; reading of SURVEY §8(c) D7):

@@ -87,7 +87,7 @@ int v2d_build_pyramid(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, in
 int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int W, int H,
                     int grid_x, int grid_y, int k, int K_min, float min_score, int border,
                     int nms, float* kp_xy, float* kp_score, int32_t* cell_count, float* resp,
-                    const uint8_t* const* mask_ptrs, const int32_t* enable,
+                    float* workspace, const uint8_t* const* mask_ptrs, const int32_t* enable,
                     v2d_stream_t stream) {
   int kk = 0;
   if (B < 0 || B > 65535) return V2D_EINVAL;
@@ -102,6 +102,9 @@ int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int 
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
   if (l0_pitch * (int64_t)H >= ((int64_t)1 << 31)) return V2D_EINVAL;  // 32-bit row offsets
   v2d::GfttArgs a{W, H, grid_x, grid_y, kk, border, nms, min_score, l0_pitch};
+  if (workspace)
+    return v2d::launch_gftt_dense(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp, workspace,
+                                  mask_ptrs, enable, reinterpret_cast<cudaStream_t>(stream));
   return v2d::launch_gftt(l0_ptrs, B, a, kp_xy, kp_score, cell_count, resp, mask_ptrs, enable,
                           reinterpret_cast<cudaStream_t>(stream));
 }

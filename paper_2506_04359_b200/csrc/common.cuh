@@ -50,6 +50,9 @@ int launch_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs, 
                    int B, const Levels& lv, const float* pts, int P, int patch, float* out,
                    cudaStream_t st);
 
+int launch_gftt_dense(const uint8_t* const* l0_ptrs, int B, const GfttArgs& a, float* kp_xy,
+                      float* kp_score, int32_t* cell_count, float* resp, float* ws,
+                      const uint8_t* const* mask_ptrs, const int32_t* enable, cudaStream_t st);
 int launch_suppress(uint8_t* const* mask_ptrs, int64_t pitch, int B, int W, int H,
                     const float* tracks, const uint8_t* status, int P, float min_sep,
                     const int32_t* enable, cudaStream_t st);

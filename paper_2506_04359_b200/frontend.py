@@ -45,6 +45,9 @@ class Frontend2D:
         self.status = torch.zeros((self.B, self.P), dtype=torch.uint8, device=d)
         self.ncc = torch.zeros((self.B, self.P), dtype=torch.float32, device=d)
         self.iters = torch.zeros((self.B, self.P), dtype=torch.int32, device=d)
+        # K2 workspace (dense two-pass detection): B*H*W floats
+        self.ws = torch.empty((self.B, cfg.H, v2d.workspace_pitch(cfg.W)), dtype=torch.float32,
+                              device=d)
         # pyramid pointer tables per parity: current and previous images
         cur, prev = [], []
         for par in (0, 1):
@@ -74,7 +77,7 @@ class Frontend2D:
             events[1].record()
         v2d.detect_gftt_ptrs(l0_ptrs, self.pitch, B, W, H, c.grid_x, c.grid_y, c.k, c.K_min,
                              c.min_score, c.border, c.nms, self.kp_xy[1:], self.kp_score[1:],
-                             self.cell_count[1:])
+                             self.cell_count[1:], workspace=self.ws)
         if events is not None:
             events[2].record()
         st = self.status if status_out is None else status_out
@@ -95,7 +98,7 @@ class Frontend2D:
         v2d.build_pyramid_ptrs(l0_ptrs_last, self.pitch, C, c.W, c.H, c.levels, pyr_ptrs)
         v2d.detect_gftt_ptrs(l0_ptrs_last, self.pitch, C, c.W, c.H, c.grid_x, c.grid_y, c.k,
                              c.K_min, c.min_score, c.border, c.nms, self.kp_xy[0],
-                             self.kp_score[0], self.cell_count[0])
+                             self.kp_score[0], self.cell_count[0], workspace=self.ws)
 
 
 class RingSchedule:
@@ -163,6 +166,7 @@ class KeyframeTracker:
         self.track_id = torch.full((C, P), -1, dtype=torch.int32, device=d)
         self.next_id = torch.zeros((C,), dtype=torch.int32, device=d)
         self.mask = torch.zeros((C, cfg.H, l0_pitch), dtype=torch.uint8, device=d)
+        self.ws = torch.empty((C, cfg.H, v2d.workspace_pitch(cfg.W)), dtype=torch.float32, device=d)
         self.mask_ptrs = v2d.ptrs_of(self.mask)
         self.kp_xy = torch.full((C, cfg.grid_y, cfg.grid_x, self.k, 2), -1.0, device=d)
         self.kp_score = torch.zeros((C, cfg.grid_y, cfg.grid_x, self.k), device=d)
@@ -180,7 +184,7 @@ class KeyframeTracker:
                                self.mask_ptrs, self.pitch, self.flag)
         v2d.detect_gftt_ptrs(l0_ptrs, self.pitch, C, c.W, c.H, c.grid_x, c.grid_y, c.k, c.K_min,
                              c.min_score, c.border, c.nms, self.kp_xy, self.kp_score,
-                             self.cell_count, None, self.mask_ptrs, self.flag)
+                             self.cell_count, None, self.mask_ptrs, self.flag, self.ws)
         v2d.refill_tracks(self.kp_xy, self.cell_count, c.grid_x, c.grid_y, self.k, self.flag,
                           self.tracks[j], self.status[j], self.kf_member, self.track_id,
                           self.next_id)

@@ -56,7 +56,7 @@ def load() -> ctypes.CDLL:
     L.v2d_grid_k.argtypes = [i, i, i, i, ctypes.POINTER(ctypes.c_int)]
     L.v2d_build_pyramid.argtypes = [vp, i64, i, i, i, i, vp, vp]
     L.v2d_detect_gftt.argtypes = [vp, i64, i, i, i, i, i, i, i, f, i, i, vp, vp, vp, vp, vp, vp,
-                                  vp]
+                                  vp, vp]
     L.v2d_suppress_mask.argtypes = [vp, vp, i, i, f, i, i, vp, i64, vp, vp]
     L.v2d_track_survival.argtypes = [vp, vp, i, i, vp, vp]
     L.v2d_keyframe_decide.argtypes = [vp, i, f, vp, vp, vp]
@@ -132,13 +132,21 @@ def build_pyramid_ptrs(l0_ptrs, l0_pitch, B, W, H, levels, pyr_ptrs):
                                     _stream()), "build_pyramid")
 
 
+def workspace_pitch(W: int) -> int:
+    """Row pitch (floats) of the dense-detection workspace."""
+    return (W + 31) // 32 * 32
+
+
 def detect_gftt_ptrs(l0_ptrs, l0_pitch, B, W, H, grid_x, grid_y, k, K_min, min_score, border,
-                     nms, kp_xy, kp_score, cell_count, resp=None, mask_ptrs=None, enable=None):
-    _need_cuda(kp_xy, kp_score, cell_count, resp, enable)
+                     nms, kp_xy, kp_score, cell_count, resp=None, mask_ptrs=None, enable=None,
+                     workspace=None):
+    _need_cuda(kp_xy, kp_score, cell_count, resp, enable, workspace)
+    if workspace is not None and workspace.numel() < B * H * workspace_pitch(W):
+        raise V2DError("detect_gftt: workspace needs B*H*round_up(W,32) floats")
     _check(load().v2d_detect_gftt(_p(l0_ptrs), l0_pitch, B, W, H, grid_x, grid_y, k, K_min,
                                   float(min_score), border, nms, _p(kp_xy), _p(kp_score),
-                                  _p(cell_count), _p(resp), _p(mask_ptrs), _p(enable),
-                                  _stream()), "detect_gftt")
+                                  _p(cell_count), _p(resp), _p(workspace), _p(mask_ptrs),
+                                  _p(enable), _stream()), "detect_gftt")
 
 
 def track_klt_ptrs(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, l0_pitch, B, W, H,
@@ -176,7 +184,8 @@ def build_pyramid(frames: torch.Tensor, W: int, levels: int, out: torch.Tensor |
 
 def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int = 0,
                 K_min: int = 0, min_score: float = 0.0, border: int = 11, nms: int = 1,
-                want_resp: bool = False, mask: torch.Tensor | None = None):
+                want_resp: bool = False, mask: torch.Tensor | None = None,
+                dense: bool = True):
     """-> (kp_xy [B,gy,gx,k,2], kp_score [B,gy,gx,k], cell_count [B,gy*gx], resp|None)."""
     B, H, pitch = _frames(frames)
     kk = grid_k(grid_x, grid_y, k, K_min)
@@ -187,8 +196,10 @@ def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int =
     resp = torch.empty((B, H, W), dtype=torch.float32, device=dev) if want_resp else None
     if mask is not None and (mask.shape != frames.shape or mask.dtype != torch.uint8):
         raise V2DError("mask must be uint8 with the frames' shape [B, H, pitch]")
+    ws = torch.empty((B, H, workspace_pitch(W)), dtype=torch.float32, device=dev) if dense else None
     detect_gftt_ptrs(ptrs_of(frames), pitch, B, W, H, grid_x, grid_y, k, K_min, min_score,
-                     border, nms, xy, sc, cnt, resp, None if mask is None else ptrs_of(mask))
+                     border, nms, xy, sc, cnt, resp, None if mask is None else ptrs_of(mask),
+                     None, ws)
     return xy, sc, cnt, resp
 
 

@@ -80,10 +80,10 @@ def test_validation_without_gpu(v2d):
     assert L.v2d_build_pyramid(N, 64, 0, 64, 64, 9, N, N) == -1
     assert L.v2d_build_pyramid(N, 40, 0, 33, 10, 2, N, N) == -2
     # detect: border < 3, Eq. 1 violation, nms not 0/1, grid cell < 1 px
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 2, 1, N, N, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 256, 0.0, 3, 1, N, N, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 3, 2, N, N, N, N, N, N, N) == -1
-    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 65, 8, 4, 0, 0.0, 3, 1, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 2, 1, N, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 256, 0.0, 3, 1, N, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 8, 8, 4, 0, 0.0, 3, 2, N, N, N, N, N, N, N, N) == -1
+    assert L.v2d_detect_gftt(N, 64, 0, 64, 64, 65, 8, 4, 0, 0.0, 3, 1, N, N, N, N, N, N, N, N) == -1
     # klt: even window, window too large, iters < 1, bad pitch
     args = dict(eps=0.01, ncc=0.8, eig=0.01)
     f = ctypes.c_float

@@ -56,11 +56,12 @@ def test_pyramid_unaligned_pitch_rejected():
 
 
 # ---------------------------------------------------------- response/select
+@pytest.mark.parametrize("dense", [True, False])
 @pytest.mark.parametrize("W,H,seed", [(160, 120, 0), (97, 61, 1), (752, 480, 2)])
-def test_response_bit_exact(W, H, seed):
+def test_response_bit_exact(W, H, seed, dense):
     fr, _ = _stream(W, H, 2, seed)
     d = _to_dev(fr)
-    _, _, _, resp = v2d.detect_gftt(d, W, 4, 3, k=8, border=3, want_resp=True)
+    _, _, _, resp = v2d.detect_gftt(d, W, 4, 3, k=8, border=3, want_resp=True, dense=dense)
     resp = resp.cpu().numpy()
     for b in range(fr.shape[0]):
         R, _ = oracle.response(fr[b])
@@ -80,12 +81,13 @@ SELECT_CASES = [
 ]
 
 
+@pytest.mark.parametrize("dense", [True, False])
 @pytest.mark.parametrize("W,H,gx,gy,k,K,border,nms,ms", SELECT_CASES)
-def test_selection_bit_exact(W, H, gx, gy, k, K, border, nms, ms):
+def test_selection_bit_exact(W, H, gx, gy, k, K, border, nms, ms, dense):
     fr, _ = _stream(W, H, 3, W + H)
     d = _to_dev(fr)
     xy, sc, cnt, _ = v2d.detect_gftt(d, W, gx, gy, k=k, K_min=K, border=border, nms=nms,
-                                     min_score=ms)
+                                     min_score=ms, dense=dense)
     xy, sc, cnt = xy.cpu().numpy(), sc.cpu().numpy(), cnt.cpu().numpy()
     for b in range(fr.shape[0]):
         oxy, osc, ocnt = oracle.detect_gftt(fr[b], gx, gy, k=k, K_min=K, min_score=ms,
@@ -106,6 +108,8 @@ def test_selection_special_images():
     fr = np.stack([const, ties, corner])
     d = _to_dev(fr)
     xy, sc, cnt, _ = v2d.detect_gftt(d, W, 2, 2, k=40, border=3)
+    xy2, sc2, cnt2, _ = v2d.detect_gftt(d, W, 2, 2, k=40, border=3, dense=False)
+    assert torch.equal(xy, xy2) and torch.equal(sc, sc2) and torch.equal(cnt, cnt2)
     for b in range(3):
         oxy, osc, ocnt = oracle.detect_gftt(fr[b], 2, 2, k=40, border=3)
         assert np.array_equal(xy[b].cpu().numpy(), oxy)
