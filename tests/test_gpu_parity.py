@@ -313,3 +313,18 @@ def test_keyframe_tracker_stepwise_parity():
             assert np.array_equal(kf1[c], okf) and int(nid1[c]) == onid
             assert np.array_equal(tr1[c][refilled[c]], otr[refilled[c]])
     assert n_kf_frames >= 1
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_selection_massive_ties(dense):
+    """Thousands of exactly equal responses in one cell (periodic pattern):
+    exercises the dense select's tie fallback and the fused kernel's folds."""
+    tile = np.zeros((8, 8), np.uint8)
+    tile[2:6, 2:6] = 200
+    img = np.tile(tile, (64, 64))  # 512 x 512
+    d = _to_dev(img[None])
+    xy, sc, cnt, _ = v2d.detect_gftt(d, 512, 1, 1, k=256, border=3, dense=dense)
+    oxy, osc, ocnt = oracle.detect_gftt(img, 1, 1, k=256, border=3)
+    assert np.array_equal(cnt[0].cpu().numpy(), ocnt)
+    assert np.array_equal(xy[0].cpu().numpy(), oxy)
+    assert np.array_equal(sc[0].cpu().numpy(), osc)
