@@ -15,16 +15,17 @@
 //     NCC(T, S(J_L, c+d+.)) < ncc_min -> LOST_NCC;  d *= 2 (L > 0)
 //   p' = p + d must lie in the half-window margin.
 //
-// B200 mapping (DESIGN.md §5 K3): one WARP per keypoint slot, lane u = window
-// column u.  Per level the warp stages a clamped 32-wide patch of the previous
-// level (template) and then of the next level (with a margin of M px for the
-// Gauss-Newton motion) into its own shared-memory tile, so the inner loops have
-// no clamping or address arithmetic (immediate smem offsets).  T, Tx, Ty stay in
-// registers as row PAIRS; every inner loop runs on packed fp32x2 FMA
-// (__ffma2_rn / FFMA2, new on sm_100) two window rows per instruction.  G, b
-// and the NCC moments are butterfly-reduced (bit-identical in every lane ->
-// warp-uniform control flow); the 2x2 solve and tests run in float64 on the
-// reduced scalars.
+// B200 mapping (DESIGN.md §5 K3): one WARP per keypoint slot.  Per level the
+// warp stages a clamped 32-wide patch of the previous level (template) and then
+// of the next level (with a margin of M px for the Gauss-Newton motion) into its
+// own shared-memory tile, so the inner loops have no clamping or address
+// arithmetic (immediate smem offsets).  The window is cut into vertical runs of
+// RL rows dealt two per lane (Tmpl: 63 runs of 7 rows for 21x21, 98% of the
+// lane slots used); T, Tx, Ty stay in registers as float2 (run .x, run .y) and
+// every inner loop runs on packed fp32x2 FMA (__ffma2_rn / FFMA2, new on
+// sm_100).  The patch pitch puts the 32 runs of a half-warp in 32 distinct
+// banks.  G, b and the NCC moments are butterfly-reduced (bit-identical in every
+// lane -> warp-uniform control flow).
 #include "common.cuh"
 
 namespace v2d {
@@ -32,14 +33,36 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kPitch = 32;  // smem row pitch (floats); lane = column
+constexpr int kGP = 32;  // gradient-grid row pitch (floats); lane = grid column
 
-// Per-warp shared memory: one 32x32 patch (template source, then the next-level
-// search patch) + the two (WIN+1)-row gradient grids of the template.
+// Window run layout (see Tmpl below): run length RL (odd, so that the patch
+// pitch below exists) = the shortest with WIN * ceil(WIN/RL) <= 64 runs.
+constexpr int run_len(int win) {
+  int rl = (win * win + 63) / 64;
+  while (win * ((win + rl - 1) / rl) > 64 || rl % 2 == 0) ++rl;
+  return rl;
+}
+constexpr int inv_mod32(int a) {
+  for (int x = 1; x < 32; x += 2)
+    if ((a * x) % 32 == 1) return x;
+  return 0;
+}
+constexpr int tile_floats(int win, int pitch) { return 32 * pitch + 2 * (win + 1) * kGP; }
+// Patch row pitch: RL * P == WIN (mod 32) puts run j (column-major) in bank
+// j mod 32, so the 32 lanes of every run-addressed LDS hit 32 distinct banks;
+// 32 (bank conflicts) if that tile would not fit 16 warps per SM.
+constexpr int patch_pitch(int win) {
+  const int p = 32 + (win * inv_mod32(run_len(win))) % 32;
+  return 64 * tile_floats(win, p) + 4 * 1024 <= 228 * 1024 ? p : 32;
+}
+
+// Per-warp shared memory: one 32-row patch (template source, then the
+// next-level search patch) + the two (WIN+1)-row gradient grids of the template.
 template <int WIN>
 struct Smem {
-  static constexpr int PATCH = 32 * kPitch;
-  static constexpr int GRID = (WIN + 1) * kPitch;
+  static constexpr int P = patch_pitch(WIN);
+  static constexpr int PATCH = 32 * P;
+  static constexpr int GRID = (WIN + 1) * kGP;
   static constexpr int TOTAL = PATCH + 2 * GRID;
 };
 
@@ -79,8 +102,9 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
 }
 
-__device__ __noinline__ void stage_f32(float* __restrict__ sp, const float* __restrict__ base,
-                                       int64_t pitch, int W, int H, int ox, int oy, int nr) {
+__device__ __noinline__ void stage_f32(float* __restrict__ sp, int kPitch,
+                                       const float* __restrict__ base, int64_t pitch, int W,
+                                       int H, int ox, int oy, int nr) {
   const int lane = threadIdx.x & 31;
   const float* col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
@@ -95,8 +119,9 @@ __device__ __noinline__ void stage_f32(float* __restrict__ sp, const float* __re
   __syncwarp();
 }
 
-__device__ __noinline__ void stage_u8(float* __restrict__ sp, const uint8_t* __restrict__ base,
-                                      int64_t pitch, int W, int H, int ox, int oy, int nr) {
+__device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
+                                      const uint8_t* __restrict__ base, int64_t pitch, int W,
+                                      int H, int ox, int oy, int nr) {
   const int lane = threadIdx.x & 31;
   const uint8_t* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
@@ -112,12 +137,14 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, const uint8_t* __r
   __syncwarp();
 }
 
-__device__ __forceinline__ void stage(float* __restrict__ sp, const Plane& pl, int ox, int oy,
-                                      int nr) {
+__device__ __forceinline__ void stage(float* __restrict__ sp, int sp_pitch, const Plane& pl,
+                                      int ox, int oy, int nr) {
   if (pl.u8)
-    stage_u8(sp, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
+    stage_u8(sp, sp_pitch, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox,
+             oy, nr);
   else
-    stage_f32(sp, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
+    stage_f32(sp, sp_pitch, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox,
+              oy, nr);
 }
 
 struct LevelOut {
@@ -127,27 +154,74 @@ struct LevelOut {
   int levels;  // levels whose template was built
 };
 
-// Template rows in split pairs: .x = window row p, .y = window row p + H2 - 1
-// (H2 = (WIN+1)/2); the y-copy of the shared middle row (p = 0) is zeroed.
+// Window run layout.  Every window column is cut into K vertical runs of RL
+// rows; run k of column c starts at row min(k*RL, WIN-RL) (the last run is
+// shifted up to end on row WIN-1 and its first `skip` rows, which repeat rows
+// of the previous run, are masked).  The WIN*K <= 64 runs, in column-major
+// order j = k*WIN + c, are dealt to the warp two per lane: run j = lane is the
+// .x half and run j = lane+32 the .y half of every packed float2.  A 21x21
+// window is 63 runs of 7 rows (448 slots for 441 pixels) where one column per
+// lane would need 21 lanes x 22 rows; with the patch pitch P of Smem the 32
+// runs of a half sit in 32 distinct banks.
 template <int WIN>
 struct Tmpl {
-  static constexpr int H2 = (WIN + 1) / 2;
-  float2 T[H2], TX[H2], TY[H2];
+  static constexpr int RL = run_len(WIN);
+  static constexpr int K = (WIN + RL - 1) / RL;
+  static constexpr bool kExact = K * RL == WIN;  // no shifted run: skip is 0 or RL
+  float2 T[RL], TX[RL], TY[RL];
+};
+
+// Run j -> window column, first window row and first valid slot (RL = unused
+// run; it repeats the address of the last run, a broadcast, and is masked).
+template <int WIN>
+__device__ __forceinline__ void run_of(int j, int& col, int& r0, int& skip) {
+  constexpr int RL = Tmpl<WIN>::RL, K = Tmpl<WIN>::K;
+  const bool used = j < WIN * K;
+  if (!used) j = WIN * K - 1;
+  const int k = j / WIN;
+  col = j - k * WIN;
+  r0 = min(k * RL, WIN - RL);
+  skip = used ? k * RL - r0 : RL;
+}
+
+// This lane's two runs: patch offsets of the run origins relative to the window
+// origin, and the slot masks.
+template <int WIN>
+struct Runs {
+  static constexpr int P = Smem<WIN>::P;
+  int offx, offy;  // r0 * P + col
+  int skx, sky;
+  __device__ __forceinline__ Runs() {
+    const int lane = threadIdx.x & 31;
+    int cx, rx, cy, ry;
+    run_of<WIN>(lane, cx, rx, skx);
+    run_of<WIN>(lane + 32, cy, ry, sky);
+    offx = rx * P + cx;
+    offy = ry * P + cy;
+  }
+  __device__ __forceinline__ float2 mask(int p) const {
+    if (Tmpl<WIN>::kExact)
+      return f2(skx == 0 ? 1.f : 0.f, sky == 0 ? 1.f : 0.f);
+    return f2(p >= skx ? 1.f : 0.f, p >= sky ? 1.f : 0.f);
+  }
 };
 
 // D7 template at one level from the staged previous-level patch P
 // (P[r][c] = I~(ix-R-1+c, iy-R-1+r)).  Gradient grids GX/GY (grid point
 // (c, g) <-> pixel (ix-R+c, iy-R+g)) hold the clamp-to-edge Sobel/8 gradient
 // IMAGE sampled with clamped coordinates, exactly as the oracle samples it.
+// Slot (run, p) is window pixel (col, r0 + p); masked slots are zeroed.
 template <int WIN>
 __device__ __forceinline__ void build_template(const float* __restrict__ P,
                                                float* __restrict__ GX, float* __restrict__ GY,
                                                int ix, int iy, float ax, float ay, int W, int H,
-                                               Tmpl<WIN>& t) {
+                                               const Runs<WIN>& ru, Tmpl<WIN>& t) {
   constexpr int R = (WIN - 1) / 2;
-  constexpr int H2 = Tmpl<WIN>::H2;
+  constexpr int RL = Tmpl<WIN>::RL;
+  constexpr int kPitch = Smem<WIN>::P;
   const int lane = threadIdx.x & 31;
-  const int c = min(lane, WIN);
+  const float* Px = P + ru.offx;
+  const float* Py = P + ru.offy;
   if ((ix - R >= 0) && (ix + R + 1 <= W - 1) && (iy - R >= 0) && (iy + R + 1 <= H - 1)) {
     // Every grid centre is inside the image, so bilinear(Sobel/8) is the
     // separable 4x4 filter: with patch columns P0..P3 = P[.][u..u+3],
@@ -155,18 +229,17 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
     //   Tx(v) = [(1-ay)V(v) + ay V(v+1)]/8,     V(v) = Dx(v) + 2Dx(v+1) + Dx(v+2)
     //   Ty(v) = [(1-ay)E(v) + ay E(v+1)]/8,     E(v) = Hs(v+2) - Hs(v)
     //   T(v)  = (1-ay)h(v+1) + ay h(v+2),       h = (1-ax)P1 + ax P2
-    // over patch rows (v = patch row - 3); rows in split pairs (q, q+H2-1).
-    const int u = min(lane, WIN - 1);
+    // swept down each run (v = run row).
     const float2 wx = f2(ax, ax), wy = f2(ay, ay), two = f2(2.f, 2.f);
     const float2 eighth = f2(0.125f, 0.125f);
-    float2 dx0 = f2(0.f, 0.f), dx1 = dx0, dx2 = dx0;   // Dx rows q-3..q-1
-    float2 hs0 = dx0, hs1 = dx0, hs2 = dx0;            // Hs rows q-3..q-1
-    float2 h1 = dx0, h2 = dx0;                         // h rows q-2, q-1
-    float2 vprev = dx0, eprev = dx0;
+    float2 dx1 = f2(0.f, 0.f), dx2 = dx1;   // Dx rows q-2, q-1
+    float2 hs1 = dx1, hs2 = dx1;            // Hs rows q-2, q-1
+    float2 h1 = dx1, h2 = dx1;              // h rows q-2, q-1
+    float2 vprev = dx1, eprev = dx1;
 #pragma unroll
-    for (int q = 0; q < H2 + 3; ++q) {
-      const float* ra = P + q * kPitch + u;
-      const float* rb = P + (q + H2 - 1) * kPitch + u;
+    for (int q = 0; q < RL + 3; ++q) {
+      const float* ra = Px + q * kPitch;
+      const float* rb = Py + q * kPitch;
       const float2 p0 = f2(ra[0], rb[0]), p1 = f2(ra[1], rb[1]);
       const float2 p2 = f2(ra[2], rb[2]), p3 = f2(ra[3], rb[3]);
       const float2 d0 = sub2(p2, p0), d1 = sub2(p3, p1);
@@ -178,50 +251,56 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       const float2 vq = fma2(two, dx2, add2(dx1, dx));
       const float2 eq = sub2(hs, hs1);
       if (q >= 3) {
-        const int pq = q - 3;  // output pair index (rows v = q-3 and q-3+H2-1)
+        const int pq = q - 3;
         t.T[pq] = fma2(wy, sub2(h2, h1), h1);
         t.TX[pq] = mul2(fma2(wy, sub2(vq, vprev), vprev), eighth);
         t.TY[pq] = mul2(fma2(wy, sub2(eq, eprev), eprev), eighth);
       }
       vprev = vq;
       eprev = eq;
-      dx0 = dx1; dx1 = dx2; dx2 = dx;
-      hs0 = hs1; hs1 = hs2; hs2 = hs;
+      dx1 = dx2; dx2 = dx;
+      hs1 = hs2; hs2 = hs;
       h1 = h2; h2 = h;
     }
   } else {
     // near a border: the gradient image is clamped, so build the clamped
     // gradient grids (grid point (c, g) <-> pixel (ix-R+c, iy-R+g), sampled at
-    // the clamped centre) and interpolate them
+    // the clamped centre; lane = grid column) and interpolate them
+    const int c = min(lane, WIN);
     const int lc = clampi(ix - R + c, 0, W - 1) - (ix - R - 1);
     for (int g = 0; g <= WIN; ++g) {
       const int lr = clampi(iy - R + g, 0, H - 1) - (iy - R - 1);
       const float* up = P + (lr - 1) * kPitch;
       const float* md = P + lr * kPitch;
       const float* dn = P + (lr + 1) * kPitch;
-      GX[g * kPitch + lane] = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
+      GX[g * kGP + lane] = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
                                (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1])) * 0.125f;
-      GY[g * kPitch + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
+      GY[g * kGP + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
                                (up[lc - 1] + 2.f * up[lc] + up[lc + 1])) * 0.125f;
     }
     __syncwarp();
-    // T row v from patch rows v+1, v+2 / cols u+1, u+2; Tx, Ty row v from grid
+    // T slot (v, u) from patch rows v+1, v+2 / cols u+1, u+2; Tx, Ty from grid
     // rows v, v+1 / cols u, u+1 (shared bilinear weights)
-    const int u = min(lane, WIN - 1);
     const float2 wx = f2(ax, ax), wy = f2(ay, ay);
-    auto hrow = [&](const float* base, int ra, int rb, int col) {
-      const float2 a0 = f2(base[ra * kPitch + col], base[rb * kPitch + col]);
-      const float2 a1 = f2(base[ra * kPitch + col + 1], base[rb * kPitch + col + 1]);
+    int gcx, grx, gcy, gry, sk;
+    run_of<WIN>(lane, gcx, grx, sk);
+    run_of<WIN>(lane + 32, gcy, gry, sk);
+    const int gox = grx * kGP + gcx, goy = gry * kGP + gcy;  // run origins in the grids
+    auto hrow = [&](const float* base, int ox, int oy, int pitch, int row, int col) {
+      const float* bx = base + ox + row * pitch + col;
+      const float* by = base + oy + row * pitch + col;
+      const float2 a0 = f2(bx[0], by[0]);
+      const float2 a1 = f2(bx[1], by[1]);
       return fma2(wx, sub2(a1, a0), a0);
     };
-    float2 hp = hrow(P, 1, H2, u + 1);
-    float2 hx = hrow(GX, 0, H2 - 1, u);
-    float2 hy = hrow(GY, 0, H2 - 1, u);
+    float2 hp = hrow(P, ru.offx, ru.offy, kPitch, 1, 1);
+    float2 hx = hrow(GX, gox, goy, kGP, 0, 0);
+    float2 hy = hrow(GY, gox, goy, kGP, 0, 0);
 #pragma unroll
-    for (int p = 0; p < H2; ++p) {
-      const float2 np = hrow(P, p + 2, p + H2 + 1, u + 1);
-      const float2 nx = hrow(GX, p + 1, p + H2, u);
-      const float2 ny = hrow(GY, p + 1, p + H2, u);
+    for (int p = 0; p < RL; ++p) {
+      const float2 np = hrow(P, ru.offx, ru.offy, kPitch, p + 2, 1);
+      const float2 nx = hrow(GX, gox, goy, kGP, p + 1, 0);
+      const float2 ny = hrow(GY, gox, goy, kGP, p + 1, 0);
       t.T[p] = fma2(wy, sub2(np, hp), hp);
       t.TX[p] = fma2(wy, sub2(nx, hx), hx);
       t.TY[p] = fma2(wy, sub2(ny, hy), hy);
@@ -230,11 +309,9 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       hy = ny;
     }
   }
-  const float valid = lane < WIN ? 1.0f : 0.0f;
-  const float2 vv = f2(valid, valid);
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
-    const float2 m = p == 0 ? f2(valid, 0.f) : vv;
+  for (int p = 0; p < RL; ++p) {
+    const float2 m = ru.mask(p);
     t.T[p] = mul2(t.T[p], m);
     t.TX[p] = mul2(t.TX[p], m);
     t.TY[p] = mul2(t.TY[p], m);
@@ -242,24 +319,27 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
 }
 
 // sum over the window of e*(Tx, Ty), e = T - S (S bilinear of the staged
-// next-level patch at origin (lc0, lr0) with weights (bx, by)).
+// next-level patch at origin (lc0, lr0) with weights (bx, by)); masked slots
+// have T = Tx = Ty = 0 and contribute nothing.
 template <int WIN>
 __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, int lr0, float bx,
-                                         float by, const Tmpl<WIN>& t) {
-  constexpr int H2 = Tmpl<WIN>::H2;
-  const int lane = threadIdx.x & 31;
-  const float* base = JP + lr0 * kPitch + lc0 + min(lane, WIN - 1);
+                                         float by, const Runs<WIN>& ru, const Tmpl<WIN>& t) {
+  constexpr int RL = Tmpl<WIN>::RL;
+  constexpr int kPitch = Smem<WIN>::P;
+  const float* base = JP + lr0 * kPitch + lc0;
+  const float* bxp = base + ru.offx;
+  const float* byp = base + ru.offy;
   const float2 wx = f2(bx, bx), wy = f2(by, by);
-  auto hrow = [&](int ra, int rb) {
-    const float2 a0 = f2(base[ra * kPitch], base[rb * kPitch]);
-    const float2 a1 = f2(base[ra * kPitch + 1], base[rb * kPitch + 1]);
+  auto hrow = [&](int r) {
+    const float2 a0 = f2(bxp[r * kPitch], byp[r * kPitch]);
+    const float2 a1 = f2(bxp[r * kPitch + 1], byp[r * kPitch + 1]);
     return fma2(wx, sub2(a1, a0), a0);
   };
-  float2 h = hrow(0, H2 - 1);
+  float2 h = hrow(0);
   float2 ax = f2(0.f, 0.f), ay = f2(0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
-    const float2 hn = hrow(p + 1, p + H2);
+  for (int p = 0; p < RL; ++p) {
+    const float2 hn = hrow(p + 1);
     const float2 e = sub2(t.T[p], fma2(wy, sub2(hn, h), h));
     ax = fma2(e, t.TX[p], ax);
     ay = fma2(e, t.TY[p], ay);
@@ -269,27 +349,28 @@ __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, 
 }
 
 // NCC moments (sum S', sum S'^2, sum T'S') with S' = S - m, T' = T - m,
-// m = template mean (second pass of the two-pass NCC).
+// m = template mean (second pass of the two-pass NCC), over the valid slots.
 template <int WIN>
 __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int lc0, int lr0,
-                                              float bx, float by, float m, const Tmpl<WIN>& t) {
-  constexpr int H2 = Tmpl<WIN>::H2;
-  const int lane = threadIdx.x & 31;
-  const float valid = lane < WIN ? 1.0f : 0.0f;
-  const float* base = JP + lr0 * kPitch + lc0 + min(lane, WIN - 1);
+                                              float bx, float by, float m, const Runs<WIN>& ru,
+                                              const Tmpl<WIN>& t) {
+  constexpr int RL = Tmpl<WIN>::RL;
+  constexpr int kPitch = Smem<WIN>::P;
+  const float* base = JP + lr0 * kPitch + lc0;
+  const float* bxp = base + ru.offx;
+  const float* byp = base + ru.offy;
   const float2 wx = f2(bx, bx), wy = f2(by, by), mm = f2(m, m);
-  auto hrow = [&](int ra, int rb) {
-    const float2 a0 = f2(base[ra * kPitch], base[rb * kPitch]);
-    const float2 a1 = f2(base[ra * kPitch + 1], base[rb * kPitch + 1]);
+  auto hrow = [&](int r) {
+    const float2 a0 = f2(bxp[r * kPitch], byp[r * kPitch]);
+    const float2 a1 = f2(bxp[r * kPitch + 1], byp[r * kPitch + 1]);
     return fma2(wx, sub2(a1, a0), a0);
   };
-  float2 h = hrow(0, H2 - 1);
+  float2 h = hrow(0);
   float2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f), st = f2(0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
-    const float2 hn = hrow(p + 1, p + H2);
-    const float2 msk = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
-    const float2 S = mul2(sub2(fma2(wy, sub2(hn, h), h), mm), msk);
+  for (int p = 0; p < RL; ++p) {
+    const float2 hn = hrow(p + 1);
+    const float2 S = mul2(sub2(fma2(wy, sub2(hn, h), h), mm), ru.mask(p));
     s1 = add2(s1, S);
     s2 = fma2(S, S, s2);
     st = fma2(sub2(t.T[p], mm), S, st);
@@ -307,24 +388,26 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   constexpr int N = WIN * WIN;
   constexpr int M = (31 - WIN) / 2;    // staged motion margin (px)
   constexpr int SZ = WIN + 1 + 2 * M;  // staged search patch edge (<= 32)
-  constexpr int H2 = Tmpl<WIN>::H2;
+  constexpr int RL = Tmpl<WIN>::RL;
   static_assert(WIN + 3 <= 32 && SZ <= 32, "window too large for one warp");
+  static_assert(WIN * Tmpl<WIN>::K <= 64, "two runs per lane");
   const int lane = threadIdx.x & 31;
   float* GX = sp + Smem<WIN>::PATCH;
   float* GY = GX + Smem<WIN>::GRID;
 
   // ---------------- template (previous frame) -----------------------------
+  const Runs<WIN> ru;
   Tmpl<WIN> t;
   {
     const float fcx = floorf(cx), fcy = floorf(cy);
     const int ix = (int)fcx, iy = (int)fcy;
-    stage(sp, I, ix - R - 1, iy - R - 1, WIN + 3);
-    build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, t);
+    stage(sp, Smem<WIN>::P, I, ix - R - 1, iy - R - 1, WIN + 3);
+    build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, ru, t);
   }
   out.levels++;
   float2 g01 = f2(0.f, 0.f), g2s = f2(0.f, 0.f);  // (Gxx, Gxy), (Gyy, sum T)
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
+  for (int p = 0; p < RL; ++p) {
     const float2 tx = t.TX[p], ty = t.TY[p], tt = t.T[p];
     g01 = fma2(f2(tx.x, tx.x), f2(tx.x, ty.x), g01);
     g01 = fma2(f2(tx.y, tx.y), f2(tx.y, ty.y), g01);
@@ -353,12 +436,10 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   // two-pass NCC, first pass: template mean, then sum (T - mean)^2 (T itself
   // stays uncentred: the Gauss-Newton residual e = T - S needs no centring)
   const float tmean = g2s.y * (1.0f / (float)N);
-  const float valid = lane < WIN ? 1.0f : 0.0f;
   float2 q = f2(0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < H2; ++p) {
-    const float2 m = p == 0 ? f2(valid, 0.f) : f2(valid, valid);
-    const float2 d = mul2(sub2(t.T[p], f2(tmean, tmean)), m);
+  for (int p = 0; p < RL; ++p) {
+    const float2 d = mul2(sub2(t.T[p], f2(tmean, tmean)), ru.mask(p));
     q = fma2(d, d, q);
   }
   const float2 qs = warp_sum2(q);
@@ -378,7 +459,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     if (!staged || lc0 < 0 || lc0 > 2 * M || lr0 < 0 || lr0 > 2 * M) {
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
-      stage(sp, J, jx0, jy0, SZ);
+      stage(sp, Smem<WIN>::P, J, jx0, jy0, SZ);
       staged = true;
       lc0 = M;
       lr0 = M;
@@ -389,7 +470,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
-    const float2 b = warp_sum2(gn_rhs<WIN>(sp, lc0, lr0, bx, by, t));
+    const float2 b = warp_sum2(gn_rhs<WIN>(sp, lc0, lr0, bx, by, ru, t));
     const float ex = fmaf(i00, b.x, i01 * b.y);
     const float ey = fmaf(i01, b.x, i11 * b.y);
     dx += ex;
@@ -410,7 +491,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
       int lc0n, lr0n;
       float bxn, byn;
       locate(nx, ny, lc0n, lr0n, bxn, byn);
-      const float3 mo = ncc_moments<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, t);
+      const float3 mo = ncc_moments<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, ru, t);
       const float2 r1 = warp_sum2(f2(mo.x, mo.y));
       const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
       const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
@@ -428,7 +509,7 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
-    const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, tmean, t);
+    const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, tmean, ru, t);
     const float2 r1 = warp_sum2(f2(mo.x, mo.y));
     const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
     // S' = S - mean_T: sum(S-Sm)^2 = sum S'^2 - (sum S')^2/n and
@@ -456,7 +537,7 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
            const float* __restrict__ guess, const uint8_t* __restrict__ in_status,
            float* __restrict__ out_pos, uint8_t* __restrict__ status, float* __restrict__ ncc,
            int32_t* __restrict__ iters_out) {
-  __shared__ float s_mem[kWarps * Smem<WIN>::TOTAL];
+  extern __shared__ __align__(16) float s_mem[];  // kWarps * Smem<WIN>::TOTAL floats
   const int64_t warp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (warp >= (int64_t)B * a.P) return;  // warp-uniform
@@ -522,7 +603,13 @@ void launch_win(const uint8_t* const* prev_l0, const float* const* prev_pyr,
                 int32_t* iters_out, cudaStream_t st) {
   const int64_t warps = (int64_t)B * a.P;
   const unsigned blocks = (unsigned)((warps + kWarps - 1) / kWarps);
-  klt_kernel<WIN><<<blocks, kThreads, 0, st>>>(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a,
+  constexpr int smem = kWarps * Smem<WIN>::TOTAL * (int)sizeof(float);
+  static bool attr = false;  // opt in above 48 KB once per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(klt_kernel<WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  klt_kernel<WIN><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a,
                                                 pts, guess, in_status, out_pos, status, ncc,
                                                 iters_out);
 }
