@@ -63,7 +63,8 @@ struct Smem {
   static constexpr int P = patch_pitch(WIN);
   static constexpr int PATCH = 32 * P;
   static constexpr int GRID = (WIN + 1) * kGP;
-  static constexpr int TOTAL = PATCH + 2 * GRID;
+  static constexpr int SCRATCH = 32 * 36 / 4;  // u8 staging bytes (shares the grids)
+  static constexpr int TOTAL = PATCH + (2 * GRID > SCRATCH ? 2 * GRID : SCRATCH);
 };
 
 struct Plane {
@@ -119,12 +120,37 @@ __device__ __noinline__ void stage_f32(float* __restrict__ sp, int kPitch,
   __syncwarp();
 }
 
+__device__ __forceinline__ void cp_async4b(uint8_t* dst, const uint8_t* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+// u8 rows: windows needing no clamping copy 4-byte aligned words (9 per row,
+// 3 rows per instruction) into a byte scratch tile with cp.async and convert
+// in shared memory; windows at the border load clamped bytes 8 rows deep.
 __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
+                                      uint8_t* __restrict__ scratch,
                                       const uint8_t* __restrict__ base, int64_t pitch, int W,
                                       int H, int ox, int oy, int nr) {
   const int lane = threadIdx.x & 31;
-  const uint8_t* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
+  const int sh = ox & 3;
+  if (ox >= 0 && ox + 32 <= W && oy >= 0 && oy + nr <= H && ox - sh + 36 <= pitch &&
+      ((reinterpret_cast<uintptr_t>(base) | (uintptr_t)pitch) & 3) == 0) {
+    constexpr int kSP = 36;  // scratch bytes per row
+    const int w = lane % 9, rr = lane / 9;
+    const uint8_t* src = base + (int64_t)oy * pitch + (ox - sh) + 4 * w;
+    if (lane < 27)
+      for (int r = rr; r < nr; r += 3) cp_async4b(scratch + r * kSP + 4 * w, src + r * pitch);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    const uint8_t* q = scratch + sh + lane;
+#pragma unroll 8
+    for (int r = 0; r < nr; ++r) sp[r * kPitch + lane] = (float)q[r * kSP];
+    __syncwarp();
+    return;
+  }
+  const uint8_t* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
   for (int r0 = 0; r0 < nr; r0 += 8) {
     unsigned v[8];
 #pragma unroll
@@ -139,9 +165,9 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
 
 __device__ __forceinline__ void stage(float* __restrict__ sp, int sp_pitch, const Plane& pl,
                                       int ox, int oy, int nr) {
-  if (pl.u8)
-    stage_u8(sp, sp_pitch, reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox,
-             oy, nr);
+  if (pl.u8)  // byte scratch: the gradient grids behind the 32-row patch (free while staging)
+    stage_u8(sp, sp_pitch, reinterpret_cast<uint8_t*>(sp + 32 * sp_pitch),
+             reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
   else
     stage_f32(sp, sp_pitch, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox,
               oy, nr);
