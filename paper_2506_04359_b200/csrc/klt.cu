@@ -225,10 +225,16 @@ struct Runs {
     offx = rx * P + cx;
     offy = ry * P + cy;
   }
+  // per-slot mask; only used when runs are shifted (!kExact): exact layouts keep
+  // unmasked slots (an unused run repeats a valid run's values) and mask whole
+  // runs once, in the final .x/.y combine (sum2)
   __device__ __forceinline__ float2 mask(int p) const {
-    if (Tmpl<WIN>::kExact)
-      return f2(skx == 0 ? 1.f : 0.f, sky == 0 ? 1.f : 0.f);
     return f2(p >= skx ? 1.f : 0.f, p >= sky ? 1.f : 0.f);
+  }
+  // this lane's share of a per-slot sum accumulated as (run .x, run .y)
+  __device__ __forceinline__ float sum2(float2 v) const {
+    if (Tmpl<WIN>::kExact) return fmaf(v.y, sky == 0 ? 1.f : 0.f, skx == 0 ? v.x : 0.f);
+    return v.x + v.y;
   }
 };
 
@@ -335,12 +341,14 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       hy = ny;
     }
   }
+  if (!Tmpl<WIN>::kExact) {
 #pragma unroll
-  for (int p = 0; p < RL; ++p) {
-    const float2 m = ru.mask(p);
-    t.T[p] = mul2(t.T[p], m);
-    t.TX[p] = mul2(t.TX[p], m);
-    t.TY[p] = mul2(t.TY[p], m);
+    for (int p = 0; p < RL; ++p) {
+      const float2 m = ru.mask(p);
+      t.T[p] = mul2(t.T[p], m);
+      t.TX[p] = mul2(t.TX[p], m);
+      t.TY[p] = mul2(t.TY[p], m);
+    }
   }
 }
 
@@ -371,7 +379,7 @@ __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, 
     ay = fma2(e, t.TY[p], ay);
     h = hn;
   }
-  return f2(ax.x + ax.y, ay.x + ay.y);
+  return f2(ru.sum2(ax), ru.sum2(ay));
 }
 
 // NCC moments (sum S', sum S'^2, sum T'S') with S' = S - m, T' = T - m,
@@ -396,13 +404,14 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
     const float2 hn = hrow(p + 1);
-    const float2 S = mul2(sub2(fma2(wy, sub2(hn, h), h), mm), ru.mask(p));
+    float2 S = sub2(fma2(wy, sub2(hn, h), h), mm);
+    if (!Tmpl<WIN>::kExact) S = mul2(S, ru.mask(p));
     s1 = add2(s1, S);
     s2 = fma2(S, S, s2);
     st = fma2(sub2(t.T[p], mm), S, st);
     h = hn;
   }
-  return make_float3(s1.x + s1.y, s2.x + s2.y, st.x + st.y);
+  return make_float3(ru.sum2(s1), ru.sum2(s2), ru.sum2(st));
 }
 
 // One pyramid level of D7 for the warp's keypoint; (dx, dy) in level px.
@@ -431,15 +440,17 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, ru, t);
   }
   out.levels++;
-  float2 g01 = f2(0.f, 0.f), g2s = f2(0.f, 0.f);  // (Gxx, Gxy), (Gyy, sum T)
+  // per-run accumulation (.x run, .y run) -> no operand shuffling
+  float2 axx = f2(0.f, 0.f), axy = axx, ayy = axx, ats = axx;
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
-    const float2 tx = t.TX[p], ty = t.TY[p], tt = t.T[p];
-    g01 = fma2(f2(tx.x, tx.x), f2(tx.x, ty.x), g01);
-    g01 = fma2(f2(tx.y, tx.y), f2(tx.y, ty.y), g01);
-    g2s = fma2(f2(ty.x, 1.f), f2(ty.x, tt.x), g2s);
-    g2s = fma2(f2(ty.y, 1.f), f2(ty.y, tt.y), g2s);
+    axx = fma2(t.TX[p], t.TX[p], axx);
+    axy = fma2(t.TX[p], t.TY[p], axy);
+    ayy = fma2(t.TY[p], t.TY[p], ayy);
+    ats = add2(t.T[p], ats);
   }
+  float2 g01 = f2(ru.sum2(axx), ru.sum2(axy));  // (Gxx, Gxy)
+  float2 g2s = f2(ru.sum2(ayy), ru.sum2(ats));  // (Gyy, sum T)
   g01 = warp_sum2(g01);
   g2s = warp_sum2(g2s);
   // lambda_min(G)/n < min_eig  <=>  det < min_eig * n * lambda_max  (no division)
@@ -465,11 +476,11 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
   float2 q = f2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
-    const float2 d = mul2(sub2(t.T[p], f2(tmean, tmean)), ru.mask(p));
+    float2 d = sub2(t.T[p], f2(tmean, tmean));
+    if (!Tmpl<WIN>::kExact) d = mul2(d, ru.mask(p));
     q = fma2(d, d, q);
   }
-  const float2 qs = warp_sum2(q);
-  const float Stt = qs.x + qs.y;
+  const float Stt = warp_sum2(f2(ru.sum2(q), 0.f)).x;
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
   const int W = J.W, H = J.H;
