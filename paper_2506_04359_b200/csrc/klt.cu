@@ -416,9 +416,10 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
 
 // One pyramid level of D7 for the warp's keypoint; (dx, dy) in level px.
 template <int WIN>
-__device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
-                                         const int L, const float cx, const float cy, float& dx,
-                                         float& dy, const KltArgs a, LevelOut& out) {
+__device__ __forceinline__ void track_level_body(float* __restrict__ sp, const Plane& I,
+                                                 const Plane& J, const int L, const float cx,
+                                                 const float cy, float& dx, float& dy,
+                                                 const KltArgs& a, LevelOut& out) {
   constexpr int R = (WIN - 1) / 2;
   constexpr int N = WIN * WIN;
   constexpr int M = (31 - WIN) / 2;    // staged motion margin (px)
@@ -564,6 +565,22 @@ __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, 
     dx *= 2.0f;
     dy *= 2.0f;
   }
+}
+
+// Out of line (instruction-cache bound kernel); the in/out state is copied into
+// registers for the level (a by-reference noinline argument would live in local
+// memory inside the Gauss-Newton loop).
+template <int WIN>
+__device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
+                                         const int L, const float cx, const float cy,
+                                         float& dx_io, float& dy_io, const KltArgs a,
+                                         LevelOut& out_io) {
+  float dx = dx_io, dy = dy_io;
+  LevelOut out = out_io;
+  track_level_body<WIN>(sp, I, J, L, cx, cy, dx, dy, a, out);
+  dx_io = dx;
+  dy_io = dy;
+  out_io = out;
 }
 
 template <int WIN>
