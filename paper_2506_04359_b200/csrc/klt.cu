@@ -263,7 +263,6 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
     //   T(v)  = (1-ay)h(v+1) + ay h(v+2),       h = (1-ax)P1 + ax P2
     // swept down each run (v = run row).
     const float2 wx = f2(ax, ax), wy = f2(ay, ay), two = f2(2.f, 2.f);
-    const float2 eighth = f2(0.125f, 0.125f);
     float2 dx1 = f2(0.f, 0.f), dx2 = dx1;   // Dx rows q-2, q-1
     float2 hs1 = dx1, hs2 = dx1;            // Hs rows q-2, q-1
     float2 h1 = dx1, h2 = dx1;              // h rows q-2, q-1
@@ -285,8 +284,8 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       if (q >= 3) {
         const int pq = q - 3;
         t.T[pq] = fma2(wy, sub2(h2, h1), h1);
-        t.TX[pq] = mul2(fma2(wy, sub2(vq, vprev), vprev), eighth);
-        t.TY[pq] = mul2(fma2(wy, sub2(eq, eprev), eprev), eighth);
+        t.TX[pq] = fma2(wy, sub2(vq, vprev), vprev);  // 8 x bilinear(Sobel/8)
+        t.TY[pq] = fma2(wy, sub2(eq, eprev), eprev);
       }
       vprev = vq;
       eprev = eq;
@@ -306,9 +305,9 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       const float* md = P + lr * kPitch;
       const float* dn = P + (lr + 1) * kPitch;
       GX[g * kGP + lane] = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
-                               (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1])) * 0.125f;
+                               (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1]));
       GY[g * kGP + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
-                               (up[lc - 1] + 2.f * up[lc] + up[lc + 1])) * 0.125f;
+                               (up[lc - 1] + 2.f * up[lc] + up[lc + 1]));
     }
     __syncwarp();
     // T slot (v, u) from patch rows v+1, v+2 / cols u+1, u+2; Tx, Ty from grid
@@ -460,7 +459,10 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   const float dg = gxx - gyy;
   const float lmax = 0.5f * (gxx + gyy + sqrtf(fmaf(dg, dg, 4.0f * gxy * gxy)));
   const bool finite = isfinite(gxx) && isfinite(gxy) && isfinite(gyy) && isfinite(det);
-  if (!finite || !(det > 0.0f) || det < a.min_eig * (float)N * lmax) {
+  // Tx, Ty are kept as 8 x (the Sobel/8 gradient): G and det carry 64 and 4096,
+  // b carries 8; every compensation below is a power of two, so all results are
+  // bit-identical to the unscaled arithmetic.
+  if (!finite || !(det > 0.0f) || det < a.min_eig * (float)N * lmax * 64.0f) {
     if (L > 0) {
       dx *= 2.0f;
       dy *= 2.0f;
@@ -469,7 +471,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     }
     return;
   }
-  const float inv_det = 1.0f / det;
+  const float inv_det = 8.0f / det;  // (G/64)^-1 / 8 applied to 8 b
   const float i00 = gyy * inv_det, i01 = -gxy * inv_det, i11 = gxx * inv_det;
   // two-pass NCC, first pass: template mean, then sum (T - mean)^2 (T itself
   // stays uncentred: the Gauss-Newton residual e = T - S needs no centring)
@@ -484,7 +486,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   const float Stt = warp_sum2(f2(ru.sum2(q), 0.f)).x;
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
-  const int W = J.W, H = J.H;
+  const float xmax = (float)(J.W - 1), ymax = (float)(J.H - 1);
   int jx0 = 0, jy0 = 0;
   bool staged = false;
   auto locate = [&](float qx, float qy, int& lc0, int& lr0, float& bx, float& by) {
@@ -515,7 +517,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     dy += ey;
     out.steps++;
     const float nx = cx + dx, ny = cy + dy;
-    const bool inside = nx >= 0.0f && nx <= (float)(W - 1) && ny >= 0.0f && ny <= (float)(H - 1);
+    const bool inside = nx >= 0.0f && nx <= xmax && ny >= 0.0f && ny <= ymax;
     if (!inside) {  // (also false for NaN)
       if (L > 0) {
         dx -= ex;
