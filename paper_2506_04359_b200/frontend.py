@@ -9,8 +9,9 @@ index b = f*C + c):
     kp slot 0 <- kp slot F     (carry: frame t+F-1's keypoints feed the next step)
 
 Frames are addressed through device pointer tables, so a ring of rendered
-frames in HBM (bench `value`) and a two-slot staging buffer filled from pinned
-host memory (bench `e2e`) run the same three launches.  Nothing here computes
+frames in HBM (bench `value`) and the three-slot staging buffers of HostStream,
+filled from pinned host memory on a copy stream (bench `e2e`), run the same
+three launches.  Nothing here computes
 any part of the method: it allocates, builds pointer tables and calls the ABI.
 """
 from __future__ import annotations
@@ -99,6 +100,101 @@ class Frontend2D:
         v2d.detect_gftt_ptrs(l0_ptrs_last, self.pitch, C, c.W, c.H, c.grid_x, c.grid_y, c.k,
                              c.K_min, c.min_score, c.border, c.nms, self.kp_xy[0],
                              self.kp_score[0], self.cell_count[0], workspace=self.ws)
+
+
+class HostStream:
+    """Public streaming entry point for frames that live in (pinned) host memory.
+
+    Per step s the caller hands in the host batch of step s+1 and gets back the
+    host results of step s:
+
+        copy stream : wait kernels(s-1) -> H2D frames(s+1) into slot (s+1) % 3
+        main stream : wait H2D(s) -> the three launches of step s -> snapshot
+                      (D2D) of the step's keypoints, positions and statuses
+        copy stream : wait kernels(s) -> D2H of the snapshot into pinned buffers
+
+    so uploads and read-backs overlap the kernels.  Three device frame slots are
+    needed because step s reads its own frames and the last frame of step s-1;
+    two snapshot/host result sets let read-back s overlap kernels s+1."""
+
+    def __init__(self, fe: Frontend2D):
+        self.fe = fe
+        B, C, P, F = fe.B, fe.C, fe.P, fe.F
+        d = fe.dev
+        self.dbuf = torch.empty((3, B, fe.cfg.H, fe.pitch), dtype=torch.uint8, device=d)
+        self.cur_t = [v2d.ptrs_of(self.dbuf[i]) for i in range(3)]
+        self.prev_t = []
+        for i in range(3):
+            pv = torch.empty_like(self.cur_t[i])
+            pv[C:] = self.cur_t[i][:-C]
+            pv[:C] = self.cur_t[(i - 1) % 3][-C:]
+            self.prev_t.append(pv)
+        self.copy = torch.cuda.Stream(device=d)
+        self.ev_in = [torch.cuda.Event() for _ in range(3)]
+        self.ev_done = [torch.cuda.Event() for _ in range(3)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.snap_kp = torch.empty((2, F, C, P, 2), dtype=torch.float32, device=d)
+        self.snap_pos = torch.empty((2, B, P, 2), dtype=torch.float32, device=d)
+        self.snap_st = torch.empty((2, B, P), dtype=torch.uint8, device=d)
+        self.host_kp = torch.empty((2, F, C, P, 2), dtype=torch.float32, pin_memory=True)
+        self.host_pos = torch.empty((2, B, P, 2), dtype=torch.float32, pin_memory=True)
+        self.host_st = torch.empty((2, B, P), dtype=torch.uint8, pin_memory=True)
+        self.h2d_bytes_per_step = B * fe.cfg.H * fe.pitch
+        self.d2h_bytes_per_step = (self.host_kp[0].numel() * 4 + self.host_pos[0].numel() * 4 +
+                                   self.host_st[0].numel())
+
+    def upload(self, s: int, host_frames: torch.Tensor):
+        """Enqueue the H2D copy of step s's frames (pinned [B, H, pitch] u8)."""
+        k = s % 3
+        with torch.cuda.stream(self.copy):
+            if s >= 1:  # slot k was read by step s-3 (current) and s-2 (previous frame)
+                self.copy.wait_event(self.ev_done[(s - 2) % 3])
+            self.dbuf[k].copy_(host_frames, non_blocking=True)
+            self.ev_in[k].record(self.copy)
+
+    def start(self, host_frames_prev: torch.Tensor):
+        """Prime with the batch preceding step 0 (its last C frames are used)."""
+        fe = self.fe
+        with torch.cuda.stream(self.copy):
+            self.dbuf[2].copy_(host_frames_prev, non_blocking=True)
+            self.ev_in[2].record(self.copy)
+        torch.cuda.current_stream().wait_event(self.ev_in[2])
+        fe.prime(self.cur_t[2][-fe.C:], 1)
+        self.ev_done[2].record()
+        self.ev_done[1].record()
+
+    def compute(self, s: int):
+        """Enqueue step s's kernels (after its upload) and its result snapshot."""
+        fe, k, j = self.fe, s % 3, s % 2
+        cs = torch.cuda.current_stream()
+        cs.wait_event(self.ev_in[k])
+        fe.step(self.cur_t[k], self.prev_t[k], j)
+        if s >= 2:  # snapshot j is free once read-back s-2 is done
+            cs.wait_event(self.ev_out[j])
+        self.snap_kp[j].copy_(fe.kp_xy[1:], non_blocking=True)
+        self.snap_pos[j].copy_(fe.pos, non_blocking=True)
+        self.snap_st[j].copy_(fe.status, non_blocking=True)
+        self.ev_done[k].record(cs)
+
+    def download(self, s: int):
+        """Enqueue the D2H read-back of step s's results into host set s % 2."""
+        j = s % 2
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.ev_done[s % 3])
+            self.host_kp[j].copy_(self.snap_kp[j], non_blocking=True)
+            self.host_pos[j].copy_(self.snap_pos[j], non_blocking=True)
+            self.host_st[j].copy_(self.snap_st[j], non_blocking=True)
+            self.ev_out[j].record(self.copy)
+
+    def results(self, s: int):
+        """Host (kp_xy, pos, status) of step s once ev_out[s % 2] has completed."""
+        self.ev_out[s % 2].synchronize()
+        j = s % 2
+        return self.host_kp[j], self.host_pos[j], self.host_st[j]
+
+    def finish(self):
+        """Make the main stream wait for all pending copies."""
+        torch.cuda.current_stream().wait_stream(self.copy)
 
 
 class RingSchedule:

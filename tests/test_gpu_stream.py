@@ -1,0 +1,59 @@
+"""The public host-streaming API (frontend.HostStream: pipelined H2D / kernels /
+D2H on two streams) returns exactly what the device-resident frontend computes
+for the same frames, step by step (bit-identical keypoints, positions and
+statuses): the overlap changes timing only."""
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def test_host_stream_matches_device_frontend():
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import Frontend2D, HostStream
+    wl = synth.WORKLOADS["c2"]
+    C, F, steps = wl.cams, 2, 6
+    st = synth.make_stream(wl, F * (steps + 1), "cuda")
+    frames = st.frames  # [C, R, H, pitch]
+    B = F * C
+
+    def batch(s):  # batch of step s (s = -1: the priming batch), order f*C + c
+        return torch.stack([frames[c, (s + 1) * F + f] for f in range(F) for c in range(C)])
+
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    # reference: device-resident frames, one stream
+    fe_ref = Frontend2D(cfg, C, F, "cuda", wl.pitch)
+    dev_batches = [batch(s).contiguous() for s in range(-1, steps)]
+    ptrs = [v2d.ptrs_of(b) for b in dev_batches]
+    fe_ref.prime(ptrs[0][-C:], 1)
+    ref = []
+    for s in range(steps):
+        cur, prv = ptrs[s + 1], torch.empty_like(ptrs[s + 1])
+        prv[C:] = cur[:-C]
+        prv[:C] = ptrs[s][-C:]
+        fe_ref.step(cur, prv, s % 2)
+        ref.append((fe_ref.kp_xy[1:].clone(), fe_ref.pos.clone(), fe_ref.status.clone()))
+    torch.cuda.synchronize()
+    # pipelined host stream
+    host = [b.cpu().pin_memory() for b in dev_batches]
+    fe = Frontend2D(cfg, C, F, "cuda", wl.pitch)
+    hs = HostStream(fe)
+    hs.start(host[0])
+    hs.upload(0, host[1])
+    for s in range(steps):
+        if s + 1 < steps:
+            hs.upload(s + 1, host[s + 2])
+        hs.compute(s)
+        hs.download(s)
+        kp, pos, status = hs.results(s)
+        assert torch.equal(kp, ref[s][0].cpu()), s
+        assert torch.equal(pos, ref[s][1].cpu()), s
+        assert torch.equal(status, ref[s][2].cpu()), s
+    hs.finish()
+    torch.cuda.synchronize()
+    assert B == hs.h2d_bytes_per_step // (wl.H * wl.pitch)
