@@ -535,7 +535,22 @@ def run_variants(fe, sched, args, wl, F, C, reps=20):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / (n_frames - 2)
     alive = float((kt.table()[1] == 0).float().mean())
+    # the same loop replayed as CUDA graphs (frame tables gathered on the device)
+    table = sched.cur.view(-1, ring_C)  # [R, C] frame pointers, frame t = row t
+    kt.capture(table, n_frames)
+    n_g = 100  # frame t = row t % R (wraps around the ring if it is short)
+    for _ in range(2):
+        kt.replay()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(n_g - 2):
+        kt.replay()
+    b.record()
+    torch.cuda.synchronize()
+    ms_g = a.elapsed_time(b) / max(n_g - 2, 1)
     out["keyframe_tracking_f1"] = {"ms_per_rig_frame": ms, "camera_frames_per_s": C / (ms * 1e-3),
+                                   "ms_per_rig_frame_graph": ms_g,
+                                   "camera_frames_per_s_graph": C / (ms_g * 1e-3),
                                    "keyframe_rate": float(kfs.item()) / (n_frames - 2),
                                    "alive_fraction_end": alive, "T": 0.7,
                                    "min_separation_px": kt.min_sep, "launches_per_frame": 8}

@@ -313,6 +313,43 @@ class KeyframeTracker:
         self._keyframe_branch(l0_ptrs, j)
         self.cur = j
 
+    # ------------------------------------------------------------ CUDA graphs
+    def capture(self, frame_table: torch.Tensor, next_frame: int):
+        """Record the per-frame step as CUDA graphs (the loop is launch-bound: 8+
+        small launches per rig-frame).  frame_table: device int64 [R, C] frame
+        pointers, frame t = row t % R; next_frame: index of the next frame to
+        process.  The frame tables are gathered on the device from a device frame
+        counter, so replay() needs no host work besides one graph launch; one
+        graph per track-table parity.  Single-process only (group is None)."""
+        assert self.group is None, "graph capture of the multi-GPU all-reduce is not supported"
+        R = frame_table.shape[0]
+        self._ft = frame_table
+        self._t = torch.full((1,), next_frame, dtype=torch.int64, device=self.dev)
+        self._l0 = torch.empty((self.C,), dtype=torch.int64, device=self.dev)
+        self._pl0 = torch.empty((self.C,), dtype=torch.int64, device=self.dev)
+
+        def body():
+            self._l0.copy_(self._ft.index_select(0, torch.remainder(self._t, R)).view(-1))
+            self._pl0.copy_(self._ft.index_select(0, torch.remainder(self._t - 1, R)).view(-1))
+            self.step(self._l0, self._pl0)
+            self._t.add_(1)
+
+        torch.cuda.synchronize(self.dev)
+        self._graphs = {}
+        cur0 = self.cur
+        for par in (cur0, 1 - cur0):  # step() toggles self.cur during capture
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body()
+            self._graphs[par] = g
+        assert self.cur == cur0
+        torch.cuda.synchronize(self.dev)
+
+    def replay(self):
+        """One rig-frame through the captured graph of the current parity."""
+        self._graphs[self.cur].replay()
+        self.cur = 1 - self.cur
+
     def table(self):
         """(tracks [C,P,2], status [C,P], kf_member, track_id, next_id) of the current frame."""
         return (self.tracks[self.cur], self.status[self.cur], self.kf_member, self.track_id,

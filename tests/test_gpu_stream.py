@@ -57,3 +57,34 @@ def test_host_stream_matches_device_frontend():
     hs.finish()
     torch.cuda.synchronize()
     assert B == hs.h2d_bytes_per_step // (wl.H * wl.pitch)
+
+
+def test_keyframe_tracker_graph_replay_matches_eager():
+    """f1 replayed as CUDA graphs (device-side frame tables) == eager steps."""
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import KeyframeTracker
+    wl = synth.WORKLOADS["c2"]
+    C, n = wl.cams, 12
+    st = synth.make_stream(wl, n, "cuda")
+    img = st.frames.stride(1) * st.frames.element_size()
+    cam = st.frames.stride(0) * st.frames.element_size()
+    t = torch.arange(n, device="cuda", dtype=torch.int64)[:, None]
+    c = torch.arange(C, device="cuda", dtype=torch.int64)[None, :]
+    table = (st.frames.data_ptr() + c * cam + t * img).contiguous()  # [n, C]
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    eager = KeyframeTracker(cfg, C, "cuda", wl.pitch, T=0.7)
+    graph = KeyframeTracker(cfg, C, "cuda", wl.pitch, T=0.7)
+    for kt in (eager, graph):
+        kt.start(table[0])
+        kt.step(table[1], table[0])
+    for f in range(2, n):
+        eager.step(table[f], table[f - 1])
+    graph.capture(table, 2)
+    for f in range(2, n):
+        graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager.table(), graph.table()):
+        assert torch.equal(a, b)
