@@ -112,9 +112,13 @@ __device__ __noinline__ void stage_f32(float* __restrict__ sp, int kPitch,
   if (oy >= 0 && oy + nr <= H) {
     const float* p = col + (int64_t)oy * pitch;
     for (int r = 0; r < nr; ++r, p += pitch) cp_async4(sp + r * kPitch + lane, p);
-  } else {
-    for (int r = 0; r < nr; ++r)
-      cp_async4(sp + r * kPitch + lane, col + (int64_t)clampi(oy + r, 0, H - 1) * pitch);
+  } else {  // clamp-to-edge rows: advance one pitch only while the next row is inside
+    const float* p = col + (int64_t)clampi(oy, 0, H - 1) * pitch;
+    for (int r = 0; r < nr; ++r) {
+      cp_async4(sp + r * kPitch + lane, p);
+      const int y = oy + r;
+      if (y >= 0 && y < H - 1) p += pitch;
+    }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncwarp();
