@@ -266,10 +266,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; V2D_DIST_BACKEND=gloo (host-side collectives, ranks may share
+    # a GPU: no kernel waits on another rank) exists only to smoke-test this path
+    backend = os.environ.get("V2D_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     wl = synth.WORKLOADS[args.config]
     C = wl.cams
