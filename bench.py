@@ -196,6 +196,20 @@ def time_oracle(wl, seconds: float, max_frames: int = 64):
     return {"frames": n, "seconds": el, "tracked": tracked}
 
 
+# The paper's own numbers, quoted with their hardware: whole-frontend
+# track-call latencies at 768x480, context only (another path, resolution and machine).
+PAPER_CONTEXT = {
+    "note": "cuVSLAM track call (whole frontend, not detect+KLT only), 768x480; context only",
+    "rows": [
+        {"mode": "stereo (2 images)", "ms": {"RTX 4090 + i7-14700": 0.4, "Jetson AGX Orin": 1.8},
+         "cite": "PAPER.md P:255"},
+        {"mode": "2-stereo (4 images)", "ms": {"RTX 4090 + i7-14700": 0.8, "Jetson AGX Orin": 2.0},
+         "cite": "PAPER.md P:256"},
+        {"mode": "4-stereo (8 images)", "ms": {"RTX 4090 + i7-14700": 2.1}, "cite": "PAPER.md P:258"},
+    ],
+}
+
+
 def cpu_cores_used():
     return 1  # the oracle is single-threaded (plain C, no threads)
 
@@ -427,6 +441,7 @@ def main():
                      "levels_per_attempted_kp": float((iters_np >> 24).sum()) / max(attempted, 1)},
         "peaks": pk,
         "clocks": clock_rec,
+        "paper_context": PAPER_CONTEXT,
     }
     if args.extras and rank == 0:
         line["variants"] = run_variants(fe, sched, args, wl, F, C)
