@@ -277,11 +277,13 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
       const float* rb = Py + q * kPitch;
       const float2 p0 = f2(ra[0], rb[0]), p1 = f2(ra[1], rb[1]);
       const float2 p2 = f2(ra[2], rb[2]), p3 = f2(ra[3], rb[3]);
-      const float2 d0 = sub2(p2, p0), d1 = sub2(p3, p1);
-      const float2 dx = fma2(wx, sub2(d1, d0), d0);
-      const float2 s0 = fma2(two, p1, add2(p0, p2)), s1 = fma2(two, p2, add2(p1, p3));
-      const float2 hs = fma2(wx, sub2(s1, s0), s0);
+      // three horizontal lerps serve all three quantities (linearity):
+      //   Dx = l23 - l01,  Hs = l01 + 2 l12 + l23,  h = l12
+      const float2 l01 = fma2(wx, sub2(p1, p0), p0);
       const float2 h = fma2(wx, sub2(p2, p1), p1);
+      const float2 l23 = fma2(wx, sub2(p3, p2), p2);
+      const float2 dx = sub2(l23, l01);
+      const float2 hs = fma2(two, h, add2(l01, l23));
       // V(q-2) = Dx(q-2) + 2Dx(q-1) + Dx(q),  E(q-2) = Hs(q) - Hs(q-2)
       const float2 vq = fma2(two, dx2, add2(dx1, dx));
       const float2 eq = sub2(hs, hs1);
