@@ -172,6 +172,21 @@ def test_klt_stream_windows(win, levels):
     assert sum(s["both_tracked"] for s in stats) > 0.3 * pts.shape[0] * pts.shape[1]
 
 
+@pytest.mark.parametrize("win", list(range(3, 31, 2)))
+def test_klt_every_window_layout(win):
+    """Every window size (each has its own run layout: run length, exactly tiled or
+    shifted last run, bank-free patch pitch or the pitch-32 fallback) vs the
+    oracle, on a stream with motion and keypoints near the borders."""
+    W, H = 160, 120
+    levels = 3 if win <= 15 else 2
+    fr, _ = _stream(W, H, 3, 101 + win, motion=(3.0, -2.0))
+    prev, nxt = fr[:-1], fr[1:]
+    pts = np.stack([oracle.detect_gftt(f, 4, 4, k=6, border=max(3, (win - 1) // 2 + 1))[0]
+                    .reshape(-1, 2) for f in prev])
+    stats = _klt_case(prev, nxt, W, levels, pts, win=win)
+    assert sum(s["both_tracked"] for s in stats) > 0.2 * pts.shape[0] * pts.shape[1]
+
+
 def test_klt_edge_cases():
     W, H = 200, 150
     fr, _ = _stream(W, H, 2, 5)
