@@ -303,17 +303,37 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
     // near a border: the gradient image is clamped, so build the clamped
     // gradient grids (grid point (c, g) <-> pixel (ix-R+c, iy-R+g), sampled at
     // the clamped centre; lane = grid column) and interpolate them
+    // Separable and sliding down the rows: per patch row the horizontal
+    // difference d and [1 2 1] sum s at the lane's clamped column; the clamped
+    // centre row lr advances by 0 or 1 per grid row (warp-uniform).  Every value
+    // is exact in fp32 (a few multiples of 4^-L below 2^12), so the order of the
+    // sums does not matter.
     const int c = min(lane, WIN);
     const int lc = clampi(ix - R + c, 0, W - 1) - (ix - R - 1);
+    const float* col = P + lc;
+    auto row_ds = [&](int r, float& d, float& sm) {
+      const float* q = col + r * kPitch;
+      const float a = q[-1], m = q[0], e = q[1];
+      d = e - a;
+      sm = fmaf(2.f, m, a + e);
+    };
+    int lr = clampi(iy - R, 0, H - 1) - (iy - R - 1);
+    float d0, s0, d1, s1, d2, s2;  // patch rows lr-1, lr, lr+1
+    row_ds(lr - 1, d0, s0);
+    row_ds(lr, d1, s1);
+    row_ds(lr + 1, d2, s2);
     for (int g = 0; g <= WIN; ++g) {
-      const int lr = clampi(iy - R + g, 0, H - 1) - (iy - R - 1);
-      const float* up = P + (lr - 1) * kPitch;
-      const float* md = P + lr * kPitch;
-      const float* dn = P + (lr + 1) * kPitch;
-      GX[g * kGP + lane] = ((up[lc + 1] + 2.f * md[lc + 1] + dn[lc + 1]) -
-                               (up[lc - 1] + 2.f * md[lc - 1] + dn[lc - 1]));
-      GY[g * kGP + lane] = ((dn[lc - 1] + 2.f * dn[lc] + dn[lc + 1]) -
-                               (up[lc - 1] + 2.f * up[lc] + up[lc + 1]));
+      const int lrg = clampi(iy - R + g, 0, H - 1) - (iy - R - 1);
+      if (lrg != lr) {  // advanced by one row
+        d0 = d1;
+        s0 = s1;
+        d1 = d2;
+        s1 = s2;
+        row_ds(lrg + 1, d2, s2);
+        lr = lrg;
+      }
+      GX[g * kGP + lane] = fmaf(2.f, d1, d0 + d2);
+      GY[g * kGP + lane] = s2 - s0;
     }
     __syncwarp();
     // T slot (v, u) from patch rows v+1, v+2 / cols u+1, u+2; Tx, Ty from grid
