@@ -436,7 +436,7 @@ def main():
         "roofline": roof,
         "kernels": {n: {"ms_per_launch": float(k_ms[j]), "share_of_step": float(k_ms[j] / (ms / args.steps))}
                     for j, n in enumerate(names)},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": fe.launches_per_step * args.steps,
         "klt_work": {"gn_steps_per_attempted_kp": float((iters_np & 0xFFFFFF).sum()) / max(attempted, 1),
                      "levels_per_attempted_kp": float((iters_np >> 24).sum()) / max(attempted, 1)},
         "peaks": pk,

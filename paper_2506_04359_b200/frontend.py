@@ -60,7 +60,8 @@ class Frontend2D:
             pv[:cams] = other[-cams:]         # last frame of the previous step
             prev.append(pv)
         self.pyr_ptrs, self.prev_pyr_ptrs = cur, prev
-        self.launches_per_step = 3
+        # our kernels per step: pyramid, GFTT pass A + pass B (workspace path), KLT
+        self.launches_per_step = 4
 
     # ------------------------------------------------------------------
     def step(self, l0_ptrs: torch.Tensor, prev_l0_ptrs: torch.Tensor, parity: int,
