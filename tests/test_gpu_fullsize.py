@@ -99,3 +99,47 @@ def test_fullsize_tracking_quality_c2():
     e = np.concatenate(errs)
     assert len(e) > 0.8 * F * C * fe.P * 0.5
     assert np.median(e) < 0.05 and np.mean(e < 0.2) > 0.95
+
+
+def test_multistep_stream_parity_c2():
+    """Several consecutive steps of the bench configuration (pyramid parity double
+    buffer, keypoint carry from the last frame of a step to the first of the
+    next): sampled selections and tracks of every step agree with the oracle."""
+    wl = synth.WORKLOADS["c2"]
+    C, F, steps = wl.cams, 4, 4
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    st = synth.make_stream(wl, 2 * F * steps, "cuda")
+    fe = Frontend2D(cfg, C, F, "cuda", wl.pitch)
+    sched = RingSchedule(st.frames, F)
+    frames = st.frames.cpu().numpy()
+    R = frames.shape[1]
+    rng = np.random.default_rng(7)
+    fe.prime(sched.before_first, 1)
+    for s in range(steps):
+        slot0 = fe.kp_xy[0].clone()  # carry from step s-1 (overwritten by this step's carry)
+        cur, prev, parity = sched.tables(s)
+        fe.step(cur, prev, parity)
+        torch.cuda.synchronize()
+        pts_in = torch.cat([slot0[None], fe.kp_xy[1:-1]], 0)  # frame f tracks slot f
+        b = int(rng.integers(F * C))
+        f, c = divmod(b, C)
+        t = s * F + f
+        img, prv = frames[c, t % R, :, :wl.W], frames[c, (t - 1) % R, :, :wl.W]
+        oxy, osc, ocnt = oracle.detect_gftt(img, wl.grid_x, wl.grid_y, k=wl.k, K_min=wl.K_min,
+                                            border=wl.border)
+        assert np.array_equal(fe.kp_xy[1 + f, c].cpu().numpy().reshape(oxy.shape), oxy), (s, b)
+        assert np.array_equal(fe.cell_count[1 + f, c].cpu().numpy(), ocnt), (s, b)
+        _, d0 = oracle.build_pyramid(prv, wl.levels)
+        _, d1 = oracle.build_pyramid(img, wl.levels)
+        pts = pts_in[f, c].cpu().numpy().reshape(-1, 2)
+        valid = np.nonzero(pts[:, 0] >= 0)[0]
+        pick = rng.choice(valid, size=min(64, len(valid)), replace=False)
+        opos, ost, onc, dg = oracle.track_klt(d0, d1, wl.W, wl.H, wl.levels, pts[pick],
+                                              win=wl.win, iters=wl.iters, eps=wl.eps,
+                                              ncc_min=wl.ncc_min, min_eig=wl.min_eig)
+        stats = compare_klt(pts[pick], fe.pos[b].cpu().numpy()[pick],
+                            fe.status[b].cpu().numpy()[pick], opos, ost, dg)
+        assert stats["both_tracked"] > 0.5 * len(pick), (s, stats)
