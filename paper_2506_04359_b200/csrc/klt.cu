@@ -440,7 +440,9 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
 }
 
 // One pyramid level of D7 for the warp's keypoint; (dx, dy) in level px.
-template <int WIN>
+// kEachStep: variant f3 (NCC after every update), a separate instantiation so the
+// default Gauss-Newton loop carries none of its code or state.
+template <int WIN, bool kEachStep>
 __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const Plane& I,
                                                  const Plane& J, const int L, const float cx,
                                                  const float cy, float& dx, float& dy,
@@ -553,7 +555,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
       out.status = V2D_LOST_OOB;
       return;
     }
-    if (a.flags & V2D_KLT_NCC_EACH_STEP) {  // variant f3: NCC after every update
+    if (kEachStep) {  // variant f3: NCC after every update
       int lc0n, lr0n;
       float bxn, byn;
       locate(nx, ny, lc0n, lr0n, bxn, byn);
@@ -598,20 +600,20 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
 // Out of line (instruction-cache bound kernel); the in/out state is copied into
 // registers for the level (a by-reference noinline argument would live in local
 // memory inside the Gauss-Newton loop).
-template <int WIN>
+template <int WIN, bool kEachStep>
 __device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
                                          const int L, const float cx, const float cy,
                                          float& dx_io, float& dy_io, const KltArgs a,
                                          LevelOut& out_io) {
   float dx = dx_io, dy = dy_io;
   LevelOut out = out_io;
-  track_level_body<WIN>(sp, I, J, L, cx, cy, dx, dy, a, out);
+  track_level_body<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, out);
   dx_io = dx;
   dy_io = dy;
   out_io = out;
 }
 
-template <int WIN>
+template <int WIN, bool kEachStep>
 __global__ void __launch_bounds__(kThreads, 4)
 klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __restrict__ prev_pyr,
            const uint8_t* const* __restrict__ next_l0, const float* const* __restrict__ next_pyr,
@@ -654,7 +656,7 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
         I = Plane{prev_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
         J = Plane{next_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
       }
-      track_level<WIN>(sp, I, J, L, cx, cy, dx, dy, a, o);
+      track_level<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, o);
     }
   }
   float ox = -1.0f, oy = -1.0f;
@@ -688,12 +690,20 @@ void launch_win(const uint8_t* const* prev_l0, const float* const* prev_pyr,
   constexpr int smem = kWarps * Smem<WIN>::TOTAL * (int)sizeof(float);
   static bool attr = false;  // opt in above 48 KB once per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(klt_kernel<WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(klt_kernel<WIN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    cudaFuncSetAttribute(klt_kernel<WIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
     attr = true;
   }
-  klt_kernel<WIN><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a,
-                                                pts, guess, in_status, out_pos, status, ncc,
-                                                iters_out);
+  if (a.flags & V2D_KLT_NCC_EACH_STEP)
+    klt_kernel<WIN, true><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr,
+                                                          B, lv, a, pts, guess, in_status,
+                                                          out_pos, status, ncc, iters_out);
+  else
+    klt_kernel<WIN, false><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr,
+                                                           B, lv, a, pts, guess, in_status,
+                                                           out_pos, status, ncc, iters_out);
 }
 
 }  // namespace
