@@ -454,7 +454,6 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   constexpr int RL = Tmpl<WIN>::RL;
   static_assert(WIN + 3 <= 32 && SZ <= 32, "window too large for one warp");
   static_assert(WIN * Tmpl<WIN>::K <= 64, "two runs per lane");
-  const int lane = threadIdx.x & 31;
   float* GX = sp + Smem<WIN>::PATCH;
   float* GY = GX + Smem<WIN>::GRID;
 
