@@ -449,7 +449,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
                                                  const KltArgs& a, LevelOut& out) {
   constexpr int R = (WIN - 1) / 2;
   constexpr int N = WIN * WIN;
-  constexpr int M = (31 - WIN) / 2;    // staged motion margin (px)
+  constexpr int M = ((31 - WIN) / 2 < 1 ? (31 - WIN) / 2 : 1);  // staged motion margin (px)
   constexpr int SZ = WIN + 1 + 2 * M;  // staged search patch edge (<= 32)
   constexpr int RL = Tmpl<WIN>::RL;
   static_assert(WIN + 3 <= 32 && SZ <= 32, "window too large for one warp");
