@@ -47,7 +47,16 @@ constexpr int inv_mod32(int a) {
     if ((a * x) % 32 == 1) return x;
   return 0;
 }
-constexpr int tile_floats(int win, int pitch) { return 32 * pitch + 2 * (win + 1) * kGP; }
+// search margin (px) staged around the level start point; 1 measured best
+// (re-staging when the iterate leaves it is rarer than it is costly)
+__host__ __device__ constexpr int search_margin(int win) { return (31 - win) / 2 < 1 ? (31 - win) / 2 : 1; }
+// rows of the patch tile: the template patch (win+3) or the search patch
+__host__ __device__ constexpr int patch_rows(int win) {
+  return win + 3 > win + 1 + 2 * search_margin(win) ? win + 3 : win + 1 + 2 * search_margin(win);
+}
+constexpr int tile_floats(int win, int pitch) {
+  return patch_rows(win) * pitch + 2 * (win + 1) * kGP;
+}
 // Patch row pitch: RL * P == WIN (mod 32) puts run j (column-major) in bank
 // j mod 32, so the 32 lanes of every run-addressed LDS hit 32 distinct banks;
 // 32 (bank conflicts) if that tile would not fit 16 warps per SM.
@@ -61,7 +70,7 @@ constexpr int patch_pitch(int win) {
 template <int WIN>
 struct Smem {
   static constexpr int P = patch_pitch(WIN);
-  static constexpr int PATCH = 32 * P;
+  static constexpr int PATCH = patch_rows(WIN) * P;
   static constexpr int GRID = (WIN + 1) * kGP;
   static constexpr int SCRATCH = 32 * 36 / 4;  // u8 staging bytes (shares the grids)
   static constexpr int TOTAL = PATCH + (2 * GRID > SCRATCH ? 2 * GRID : SCRATCH);
@@ -167,10 +176,10 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
   __syncwarp();
 }
 
-__device__ __forceinline__ void stage(float* __restrict__ sp, int sp_pitch, const Plane& pl,
-                                      int ox, int oy, int nr) {
-  if (pl.u8)  // byte scratch: the gradient grids behind the 32-row patch (free while staging)
-    stage_u8(sp, sp_pitch, reinterpret_cast<uint8_t*>(sp + 32 * sp_pitch),
+__device__ __forceinline__ void stage(float* __restrict__ sp, int sp_pitch, float* scratch,
+                                      const Plane& pl, int ox, int oy, int nr) {
+  if (pl.u8)  // byte scratch: the gradient grids behind the patch (free while staging)
+    stage_u8(sp, sp_pitch, reinterpret_cast<uint8_t*>(scratch),
              reinterpret_cast<const uint8_t*>(pl.base), pl.pitch, pl.W, pl.H, ox, oy, nr);
   else
     stage_f32(sp, sp_pitch, reinterpret_cast<const float*>(pl.base), pl.pitch, pl.W, pl.H, ox,
@@ -449,7 +458,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
                                                  const KltArgs& a, LevelOut& out) {
   constexpr int R = (WIN - 1) / 2;
   constexpr int N = WIN * WIN;
-  constexpr int M = ((31 - WIN) / 2 < 1 ? (31 - WIN) / 2 : 1);  // staged motion margin (px)
+  constexpr int M = search_margin(WIN);  // staged motion margin (px)
   constexpr int SZ = WIN + 1 + 2 * M;  // staged search patch edge (<= 32)
   constexpr int RL = Tmpl<WIN>::RL;
   static_assert(WIN + 3 <= 32 && SZ <= 32, "window too large for one warp");
@@ -463,7 +472,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   {
     const float fcx = floorf(cx), fcy = floorf(cy);
     const int ix = (int)fcx, iy = (int)fcy;
-    stage(sp, Smem<WIN>::P, I, ix - R - 1, iy - R - 1, WIN + 3);
+    stage(sp, Smem<WIN>::P, GX, I, ix - R - 1, iy - R - 1, WIN + 3);
     build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, ru, t);
   }
   out.levels++;
@@ -526,7 +535,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     if (!staged || lc0 < 0 || lc0 > 2 * M || lr0 < 0 || lr0 > 2 * M) {
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
-      stage(sp, Smem<WIN>::P, J, jx0, jy0, SZ);
+      stage(sp, Smem<WIN>::P, GX, J, jx0, jy0, SZ);
       staged = true;
       lc0 = M;
       lr0 = M;
