@@ -609,14 +609,14 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   }
 }
 
-// Out of line (instruction-cache bound kernel); the in/out state is copied into
-// registers for the level (a by-reference noinline argument would live in local
-// memory inside the Gauss-Newton loop).
+// Inlined into the level loop (one call site, so one copy of the body; as an
+// out-of-line function its arguments and in/out state went through the stack:
+// same-box A/B -6..7 %).  The in/out state is copied into registers for the level.
 template <int WIN, bool kEachStep>
-__device__ __noinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
-                                         const int L, const float cx, const float cy,
-                                         float& dx_io, float& dy_io, const KltArgs a,
-                                         LevelOut& out_io) {
+__device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
+                                            const int L, const float cx, const float cy,
+                                            float& dx_io, float& dy_io, const KltArgs a,
+                                            LevelOut& out_io) {
   float dx = dx_io, dy = dy_io;
   LevelOut out = out_io;
   track_level_body<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, out);
