@@ -142,6 +142,14 @@ __device__ __forceinline__ void cp_async4b(uint8_t* dst, const uint8_t* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
 }
 
+// Exact byte -> fp32 as a 32-bit conversion (the compiler narrows (float)u8 to
+// I2F.U16, a multi-function-unit instruction; cvt.rn.f32.u32 is I2FP.F32.U32).
+__device__ __forceinline__ float u8_to_f32(unsigned v) {
+  float f;
+  asm("cvt.rn.f32.u32 %0, %1;" : "=f"(f) : "r"(v));
+  return f;
+}
+
 // u8 rows: windows needing no clamping copy 4-byte aligned words (9 per row,
 // 3 rows per instruction) into a byte scratch tile with cp.async and convert
 // in shared memory; windows at the border load clamped bytes 8 rows deep.
@@ -163,7 +171,7 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
     __syncwarp();
     const uint8_t* q = scratch + sh + lane;
 #pragma unroll 8
-    for (int r = 0; r < nr; ++r) sp[r * kPitch + lane] = (float)q[r * kSP];
+    for (int r = 0; r < nr; ++r) sp[r * kPitch + lane] = u8_to_f32(q[r * kSP]);
     __syncwarp();
     return;
   }
@@ -175,7 +183,7 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
       v[i] = r0 + i < nr ? __ldg(col + (int64_t)clampi(oy + r0 + i, 0, H - 1) * pitch) : 0u;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      if (r0 + i < nr) sp[(r0 + i) * kPitch + lane] = (float)v[i];
+      if (r0 + i < nr) sp[(r0 + i) * kPitch + lane] = u8_to_f32(v[i]);
   }
   __syncwarp();
 }
