@@ -118,6 +118,40 @@ def test_selection_special_images():
     assert cnt[0].sum().item() == 0
 
 
+def _extreme_images(W, H):
+    """Images at the ends of the response contract's operand ranges (DESIGN.md §5 K2:
+    det up to 2^47, D up to 2^49, det = 0 with large trace, tiny det/D)."""
+    rng = np.random.default_rng(7)
+    yy, xx = np.mgrid[0:H, 0:W]
+    return np.stack([
+        (((xx + yy) & 1) * 255).astype(np.uint8),            # 1-px checkerboard: Sobel = 0
+        ((((xx >> 1) + (yy >> 1)) & 1) * 255).astype(np.uint8),
+        (rng.integers(0, 2, (H, W)) * 255).astype(np.uint8),  # binary noise: extreme A, B, C
+        rng.integers(0, 2, (H, W)).astype(np.uint8),          # values 0/1: tiny det and D
+        ((xx * 255) // (W - 1)).astype(np.uint8),             # horizontal ramp: det = 0
+        (((xx + 2 * yy) * 3) % 256).astype(np.uint8),         # diagonal saw: rank-deficient
+        np.where(xx > yy, 255, 0).astype(np.uint8),           # saturated diagonal edge
+    ])
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_response_extreme_ranges(dense):
+    W, H = 96, 80
+    fr = _extreme_images(W, H)
+    d = _to_dev(fr)
+    _, _, _, resp = v2d.detect_gftt(d, W, 4, 3, k=8, border=3, want_resp=True, dense=dense)
+    xy, sc, cnt, _ = v2d.detect_gftt(d, W, 4, 4, k=16, border=3, dense=dense)
+    resp, xy, sc, cnt = (t.cpu().numpy() for t in (resp, xy, sc, cnt))
+    for b in range(fr.shape[0]):
+        R, _ = oracle.response(fr[b])
+        assert np.array_equal(resp[b], R), b
+        oxy, osc, ocnt = oracle.detect_gftt(fr[b], 4, 4, k=16, border=3)
+        assert np.array_equal(cnt[b], ocnt), b
+        assert np.array_equal(xy[b], oxy), b
+        assert np.array_equal(sc[b], osc), b
+    assert resp[2].max() > 3e4  # binary 0/255 noise: tensor sums near their maximum
+
+
 def test_detect_rejects_bad_k():
     d = torch.zeros((1, 64, 64), dtype=torch.uint8, device="cuda")
     with pytest.raises(v2d.V2DError):
