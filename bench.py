@@ -1,18 +1,27 @@
 #!/usr/bin/env python
 """Throughput bench of the B200 2D-frontend hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
                     [--frames-per-step F] [--impl reference]
 
-A *step* = one pass of the whole path (pyramid -> GFTT/NMS/top-k -> KLT) over
-F consecutive frames of every camera of the workload (B = F*C camera-frames),
-read from a device-resident ring of rendered frames larger than L2.  `value`
-is camera-frames/s over all ranks (max-over-ranks device time); `e2e` is the
-same metric with each step's frames copied from pinned host memory and its
-results (keypoints, tracked positions, statuses) read back inside the timed
-region.  N > 1: one process per GPU (torchrun), each rank processes its own
-frame chunk of the stream (weak scaling) and the per-step track lists are
-all-gathered over NCCL on a side stream.
+Default workload: c5, the 32-camera 1920x1200 rig the north star's targets are
+stated on (BASELINE.json configs[4]; "up to 32 cameras").  A
+*step* = one pass of the whole path (pyramid -> GFTT/NMS/top-k -> KLT, whose
+epilogue also writes the (x, y, status, ncc) track-list records) over F
+consecutive frames of the rank's cameras (B = F * cameras-per-rank = 32
+camera-frames per rank), read from a device-resident ring of rendered frames
+larger than L2.  `value` is camera-frames/s over all ranks (max-over-ranks
+device time); `e2e` is the same metric with each step's frames copied from
+pinned host memory and its results read back inside the timed region.
+
+N > 1 (one process per GPU, torchrun): ONE seeded rig stream is partitioned
+with shard.rig_shard: contiguous camera blocks (c5: 32/16/8/4
+cameras per rank at N = 1/2/4/8), or for rigs with fewer cameras than ranks one
+camera's frame chunks, each primed with the frame before it.  Per-rank work per
+step is fixed (weak scaling).  The track-list records are all-gathered over
+NCCL on a side stream once per >= 16 frames (a7), and after the timed region
+rank 0 recomputes the first steps of every rank's streams in one process and
+checks the gathered records bit for bit (`shard_check`).
 
 --impl reference times the oracle (oracle/, plain single-threaded C) on the
 host on the same workload: each step = one camera-frame.
@@ -36,7 +45,9 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 L2_BYTES = 126 * 1024 * 1024
-DEFAULT_CONFIG = "c2"
+DEFAULT_CONFIG = "c5"
+GATHER_FRAMES = 16  # frames per all-gather (B >= 16)
+VERIFY_STEPS = 2
 
 
 def parse():
@@ -56,14 +67,30 @@ def parse():
 
 
 def peaks():
+    """Roofline denominators.  HBM: MEASURED_PEAKS.json (driver-written copy
+    bandwidth).  FP32 and integer lane-op issue: profiles/alu_peaks.json, written
+    by tools/alu_peak.py on the B200 (FFMA2 / FFMA / IADD3 microbenchmarks with
+    the clocks recorded); the formula 148 SMs x 128 lanes x 2 x f_max only if
+    that file is absent (said in *_source)."""
     p = {"hbm_gbs": 6537.3, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         m = json.load(open(path))
         p.update({k: m[k] for k in ("hbm_gbs", "sm_max_mhz") if k in m})
         p["source"] = "measured (MEASURED_PEAKS.json)"
-    # FP32 CUDA-core peak: 148 SMs x 128 lanes x 2 flop/FMA x max SM clock
     p["fp32_tflops"] = 148 * 128 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    p["fp32_source"] = "formula: 148 SMs x 128 lanes x 2 flop x max SM clock"
+    p["lane_ops_tops"] = p["fp32_tflops"] / 2
+    p["lane_ops_source"] = "formula: 148 SMs x 128 lanes x max SM clock"
+    alu = os.path.join(ROOT, "profiles", "alu_peaks.json")
+    if os.path.exists(alu):
+        m = json.load(open(alu))
+        p["fp32_tflops"] = m["ffma2_tflops"]
+        p["fp32_source"] = (f"measured: FFMA2 microbenchmark ({m['ffma2_tflops']:.1f} TFLOP/s at "
+                            f"{m['clocks']['sm_mhz']:.0f} MHz), profiles/alu_peaks.json")
+        p["lane_ops_tops"] = m["iadd3_tops"]
+        p["lane_ops_source"] = (f"measured: IADD3 microbenchmark ({m['iadd3_tops']:.1f} T lane-op/s"
+                                f"), profiles/alu_peaks.json")
     return p
 
 
@@ -214,6 +241,25 @@ def cpu_cores_used():
     return 1  # the oracle is single-threaded (plain C, no threads)
 
 
+def bench_layout(wl, world: int, frames_per_step: int = 0) -> dict:
+    """Per-rank work of the ring bench, identical on every rank and in both
+    arms: streams per rank (camera blocks, or one camera's frame chunk when the
+    rig has fewer cameras than ranks), frames per step F (32 camera-frames per
+    rank and step), the ring length R (a multiple of 2F and of the chunk count,
+    and >= 2.5x L2 of frames per rank, so every step reads new frames from HBM)
+    and the steps per all-gather batch (>= 16 frames)."""
+    C = wl.cams
+    streams = max(1, C // world)
+    F = frames_per_step or max(1, 32 // streams)
+    per_cam = max(1, world // C)
+    rig_bytes = streams * wl.H * wl.pitch
+    R = max(2 * F, math.ceil(2.5 * L2_BYTES / rig_bytes))
+    m = 2 * F * per_cam // math.gcd(2 * F, per_cam)
+    R = (R + m - 1) // m * m
+    return {"streams": streams, "F": F, "R": R, "B": F * streams,
+            "gather_steps": max(1, math.ceil(GATHER_FRAMES / F))}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -221,6 +267,7 @@ def run_reference(args):
     wl = synth.WORKLOADS[args.config]
     import oracle
     oracle.build()
+    lay = bench_layout(wl, args.gpus, args.frames_per_step)
     ostream = OracleStream(wl)
     times, tracked = [], 0
     for s in range(args.warmup + args.steps):
@@ -237,12 +284,13 @@ def run_reference(args):
         "unit": "camera-frames/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(wl, 1, 1, args.gpus),
+        "data": "synthetic", "config": workload_config(wl, lay, args.gpus),
         "keypoints_tracked_per_s": tracked / total,
         "cpu_baseline": {"value": value, "unit": "camera-frames/s", "cores": cpu_cores_used(),
                          "kind": "oracle",
                          "sample": f"{args.steps} consecutive camera-frames of {wl.name} "
-                                   f"(camera 0, 8-frame cycle), one step = one camera-frame"},
+                                   f"(camera 0, 8-frame cycle), one step = one camera-frame "
+                                   f"(pyramid + detect + KLT of every slot)"},
         "e2e": {"value": value, "unit": "camera-frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -250,21 +298,50 @@ def run_reference(args):
     return 0
 
 
-def workload_config(wl, F, C, n_gpus, ring=None):
+def workload_config(wl, lay, n_gpus):
     k = wl.k or (wl.K_min // (wl.grid_x * wl.grid_y) + 1)
-    cfg = {"workload": f"{wl.name}: {wl.description}", "cams": wl.cams, "W": wl.W, "H": wl.H,
-           "levels": wl.levels, "grid": [wl.grid_x, wl.grid_y], "K_min": wl.K_min, "k": k,
-           "slots_per_image": wl.grid_x * wl.grid_y * k, "win": wl.win, "iters": wl.iters,
-           "frames_per_step": F, "images_per_step": F * C,
-           "parallelism": f"dp{n_gpus} (frame-chunk shards, one process per GPU)"}
-    if ring is not None:
-        cfg.update(ring)
-    return cfg
+    C = wl.cams
+    if C >= n_gpus:
+        par = (f"dp{n_gpus}: camera blocks of {lay['streams']} cameras per GPU, one process "
+               f"per GPU")
+    else:
+        par = (f"dp{n_gpus}: {n_gpus // C} frame chunks per camera, one camera stream per GPU, "
+               f"each chunk primed with the frame before it")
+    ring_bytes = lay["streams"] * lay["R"] * wl.H * wl.pitch
+    return {"workload": f"{wl.name}: {wl.description}", "cams": C, "W": wl.W, "H": wl.H,
+            "levels": wl.levels, "grid": [wl.grid_x, wl.grid_y], "K_min": wl.K_min, "k": k,
+            "slots_per_image": wl.grid_x * wl.grid_y * k, "win": wl.win, "iters": wl.iters,
+            "frames_per_step": lay["F"], "camera_frames_per_step_per_gpu": lay["B"],
+            "rig_frames_per_step": lay["B"] * n_gpus / C, "parallelism": par,
+            "ring_frames": lay["R"], "ring_bytes_per_gpu": ring_bytes,
+            "l2": f"inputs larger than L2: ring {ring_bytes / 2**20:.0f} MiB per GPU > 126 MiB "
+                  f"L2, each step reads new frames",
+            "track_list_gather": f"(x, y, status, ncc) records, all_gather_into_tensor every "
+                                 f"{lay['gather_steps']} steps ({lay['gather_steps'] * lay['F']} "
+                                 f"frames) on a side stream" if n_gpus > 1 else
+                                 "single GPU: records written, no collective"}
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def make_frontend(wl, streams, F, dev):
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import Frontend2D
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    return Frontend2D(cfg, streams, F, dev, wl.pitch)
+
+
+def render_streams(wl, R, shard, dev, only=None):
+    """Ring frames [cams, R, H, pitch] of the shard's cameras: the one seeded
+    rig stream (seeds depend on the camera, not the rank), so every rank holds
+    the same bytes a single process would render for those cameras."""
+    return synth.make_stream(wl, R, dev, cams=sorted(set(shard.cams)), only=only)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -273,9 +350,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2506_04359_b200 import vslam2d as v2d
-    from paper_2506_04359_b200.frontend import Frontend2D, RingSchedule
-    from paper_2506_04359_b200.shard import TrackGather
+    from paper_2506_04359_b200.frontend import RingSchedule
+    from paper_2506_04359_b200.shard import BatchedTrackGather, rig_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -294,33 +370,22 @@ def main():
 
     wl = synth.WORKLOADS[args.config]
     C = wl.cams
-    F = args.frames_per_step or max(1, 32 // C)
-    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
-                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
-                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
-                             min_eig=wl.min_eig)
-    fe = Frontend2D(cfg, C, F, dev, wl.pitch)
+    lay = bench_layout(wl, world, args.frames_per_step)
+    F, R, streams = lay["F"], lay["R"], lay["streams"]
+    shard = rig_shard(C, R, world, rank)
+    fe = make_frontend(wl, streams, F, dev)
     B, P = fe.B, fe.P
 
-    # ring of rendered frames in HBM, larger than L2 (2.5x), multiple of 2F
-    rig_bytes = C * wl.H * wl.pitch
-    R = max(2 * F, math.ceil(2.5 * L2_BYTES / rig_bytes))
-    R = (R + 2 * F - 1) // (2 * F) * (2 * F)
     t_render = time.perf_counter()
-    stream = synth.make_stream(wl, R, dev, rank_salt=rank)
+    stream = render_streams(wl, R, shard, dev)
     torch.cuda.synchronize()
     t_render = time.perf_counter() - t_render
-    sched = RingSchedule(stream.frames, F)
-    ring_info = {"ring_frames": R, "ring_bytes": int(stream.frames.numel()),
-                 "l2": f"inputs larger than L2: ring {stream.frames.numel() / 2**20:.0f} MiB "
-                       f"> 126 MiB L2, each step reads new frames"}
+    cam_idx = sorted(set(shard.cams))
+    sched = RingSchedule(stream.frames, F, cams=[cam_idx.index(c) for c in shard.cams],
+                         phases=shard.phases)
 
-    # multi-GPU: per-step track lists gathered on a side stream (double-buffered)
     side = torch.cuda.Stream(device=dev) if world > 1 else None
-    pos_buf = [torch.zeros((B, P, 2), device=dev) for _ in range(2)]
-    st_buf = [torch.zeros((B, P), dtype=torch.uint8, device=dev) for _ in range(2)]
-    gathers = [TrackGather(B, P, dev) for _ in range(2)] if world > 1 else None
-    gather_done = [None, None]
+    bg = BatchedTrackGather(lay["gather_steps"], B, P, dev, side=side)
 
     n_total = args.warmup + args.steps
     status_log = torch.zeros((args.steps, B, P), dtype=torch.uint8, device=dev)
@@ -329,41 +394,29 @@ def main():
 
     def one_step(s, timed_index=None):
         cur, prev, parity = sched.tables(s)
-        slot = s % 2
-        if world > 1 and gather_done[slot] is not None:
-            torch.cuda.current_stream().wait_event(gather_done[slot])
         evs = ev[timed_index] if timed_index is not None else None
-        fe.pos = pos_buf[slot]
-        fe.step(cur, prev, parity, status_out=st_buf[slot], events=evs)
+        fe.step(cur, prev, parity, events=evs, track_list=bg.slot(s))
         if timed_index is not None:
-            status_log[timed_index].copy_(st_buf[slot], non_blocking=True)
+            status_log[timed_index].copy_(fe.status, non_blocking=True)
             iters_log[timed_index].copy_(fe.iters, non_blocking=True)
-        if world > 1:
-            done = torch.cuda.Event()
-            done.record()
-            with torch.cuda.stream(side):
-                side.wait_event(done)
-                gathers[slot].gather(pos_buf[slot], st_buf[slot])
-                e = torch.cuda.Event()
-                e.record(side)
-                gather_done[slot] = e
+        bg.step_done(s)
 
     fe.prime(sched.before_first, 1)
     for s in range(args.warmup):
         one_step(s)
+    bg.flush()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_gathers0 = bg.n_gathers
     start.record()
     for i in range(args.steps):
         one_step(args.warmup + i, timed_index=i)
-    if world > 1:
-        for e in gather_done:
-            if e is not None:
-                torch.cuda.current_stream().wait_event(e)
+    bg.flush_partial(n_total - 1)
+    bg.flush()
     end.record()
     torch.cuda.synchronize()
     clock_rec = clocks.stop()
@@ -404,15 +457,16 @@ def main():
         ach = fl / (k_ms[dom] * 1e-3) / 1e12
         roof = {"kernel": "klt", "bound": "alu", "achieved": ach, "peak": pk["fp32_tflops"],
                 "unit": "TFLOP/s", "frac": ach / pk["fp32_tflops"], "traffic": None,
+                "peak_source": pk["fp32_source"],
                 "model": f"{KLT_FLOP_LEVEL}*n per level + {KLT_FLOP_STEP}*n per GN step, "
                          f"n=win^2, counts from the kernel's iters_out"}
     else:
         ops = B * wl.W * wl.H * 40.0
         ach = ops / (k_ms[dom] * 1e-3) / 1e12
-        peak_ops = pk["fp32_tflops"] / 2
+        peak_ops = pk["lane_ops_tops"]
         roof = {"kernel": "gftt_topk", "bound": "alu", "achieved": ach, "peak": peak_ops,
                 "unit": "Tlane-op/s", "frac": ach / peak_ops, "traffic": None,
-                "model": "40 lane-ops per L0 pixel"}
+                "peak_source": pk["lane_ops_source"], "model": "40 lane-ops per L0 pixel"}
     traffic_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(traffic_path):
         tr = json.load(open(traffic_path))
@@ -420,16 +474,20 @@ def main():
             roof["traffic"] = tr[roof["kernel"]]
     full_bytes = alg_bytes_full_path(wl.W, wl.H, wl.levels) * frames_total
     hbm_ach = full_bytes / (ms_max / 1e3) / 1e9 / world
+    rig_per_step = B * world / C
 
     line = {
         "metric": "frames/s (camera-frames, detect+KLT)", "value": value,
         "unit": "camera-frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(wl, F, C, world, ring_info),
+        "config": workload_config(wl, lay, world),
         "keypoints_tracked_per_s": tracked_all / (ms_max / 1e3),
         "keypoints_attempted_per_s": attempted_all / (ms_max / 1e3),
         "rig_frames_per_s": value / C,
+        "rig_frame_latency_ms": ms_max / args.steps,
+        "rig_frame_latency_note": f"each step completes {rig_per_step:g} rig-frame(s) "
+                                  f"({B} camera-frames on each of {world} GPU(s)) together",
         "hbm_full_path": {"achieved_GBps_per_gpu": hbm_ach, "frac_of_measured": hbm_ach / pk["hbm_gbs"],
                           "frac_of_8TBps_spec": hbm_ach / 8000.0,
                           "alg_bytes_per_camera_frame": alg_bytes_full_path(wl.W, wl.H, wl.levels)},
@@ -437,6 +495,8 @@ def main():
         "kernels": {n: {"ms_per_launch": float(k_ms[j]), "share_of_step": float(k_ms[j] / (ms / args.steps))}
                     for j, n in enumerate(names)},
         "gpu_launches": fe.launches_per_step * args.steps,
+        "collectives": {"all_gathers": bg.n_gathers - n_gathers0, "bytes_per_gather_per_rank":
+                        bg.local[0].numel() * 4} if world > 1 else None,
         "klt_work": {"gn_steps_per_attempted_kp": float((iters_np & 0xFFFFFF).sum()) / max(attempted, 1),
                      "levels_per_attempted_kp": float((iters_np >> 24).sum()) / max(attempted, 1)},
         "peaks": pk,
@@ -444,20 +504,27 @@ def main():
         "paper_context": PAPER_CONTEXT,
     }
     if args.extras and rank == 0:
-        line["variants"] = run_variants(fe, sched, args, wl, F, C)
+        line["variants"] = run_variants(fe, sched, args, wl, F, streams)
     if not args.no_e2e:
-        e2e = run_e2e(fe, stream.frames, sched, args, dev, F, C)
+        e2e = run_e2e(fe, stream.frames, sched, args, dev, F, streams)
         t = torch.tensor([e2e["ms"]], device=dev, dtype=torch.float64)
         if world > 1:
             dist.barrier()
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
+        h2d = e2e["h2d_bytes_per_step"]
         line["e2e"] = {"value": world * B * args.steps / (ms_e2e / 1e3), "unit": "camera-frames/s",
-                       "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                       "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
                        "ms_per_step": ms_e2e / args.steps, "pipelined": True,
+                       "h2d_GBps_per_gpu": h2d / (ms_e2e / args.steps * 1e-3) / 1e9,
+                       "bound": ("host->device copy (PCIe): the H2D stream of the frames takes "
+                                 "longer than the kernels" if ms_e2e / args.steps >
+                                 1.05 * ms_max / args.steps else "kernels"),
                        "api": "frontend.HostStream (H2D / D2H on a copy stream, "
                               "overlapping the kernels of neighbouring steps)"}
+    if world > 1:
+        line["shard_check"] = verify_shards(wl, lay, world, rank, fe, sched, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ob = time_oracle(wl, args.cpu_seconds)
         line["cpu_baseline"] = {
@@ -465,7 +532,8 @@ def main():
             "cores": cpu_cores_used(), "kind": "oracle",
             "sample": f"{ob['frames']} consecutive camera-frames of {wl.name} (camera 0): "
                       f"pyramid + detect + KLT of {P} slots each, {ob['seconds']:.1f} s on "
-                      f"one host core",
+                      f"one host core; camera-frames/s of the whole {C}-camera workload "
+                      f"extrapolate per camera-frame",
             "host_nproc": os.cpu_count()}
     if rank == 0:
         line["render_seconds"] = t_render
@@ -473,6 +541,61 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def verify_shards(wl, lay, world, rank, fe, sched, dev):
+    """Sharded output == single-process output (SURVEY §8(e) invariant).  Every
+    rank re-runs the first VERIFY_STEPS steps of its streams from their primes
+    and the records are all-gathered; rank 0 renders the frames of EVERY rank's
+    streams (the same seeded rig), runs them in one process (one Frontend2D over
+    all streams) and compares the gathered (x, y, status, ncc) records bit for
+    bit.  Outside the timed region."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_04359_b200.frontend import RingSchedule
+    from paper_2506_04359_b200.shard import all_gather_into, all_streams
+    V, F, R, B, P = VERIFY_STEPS, lay["F"], lay["R"], fe.B, fe.P
+    mine = torch.zeros((V, B, P, 4), dtype=torch.float32, device=dev)
+    fe.prime(sched.before_first, 1)
+    for s in range(V):
+        cur, prev, parity = sched.tables(s)
+        fe.step(cur, prev, parity, track_list=mine[s])
+    torch.cuda.synchronize()
+    allr = torch.zeros((world, V, B, P, 4), dtype=torch.float32, device=dev)
+    all_gather_into(allr, mine)
+    torch.cuda.synchronize()
+    if rank != 0:
+        return None
+    al = all_streams(wl.cams, R, world)
+    need = {(ph + t) % R for ph in al.phases for t in range(-1, V * F)}
+    t0 = time.perf_counter()
+    st = synth.make_stream(wl, R, dev, cams=sorted(set(al.cams)), only=need)
+    cam_idx = sorted(set(al.cams))
+    ref_sched = RingSchedule(st.frames, F, cams=[cam_idx.index(c) for c in al.cams],
+                             phases=al.phases)
+    nv = len(al.cams)
+    ref_fe = make_frontend(wl, nv, F, dev)
+    ref = torch.zeros((V, F * nv, P, 4), dtype=torch.float32, device=dev)
+    ref_fe.prime(ref_sched.before_first, 1)
+    for s in range(V):
+        cur, prev, parity = ref_sched.tables(s)
+        ref_fe.step(cur, prev, parity, track_list=ref[s])
+    torch.cuda.synchronize()
+    # single-process batch order f*nv + v, v = r*streams + c; rank r's is f*streams + c
+    ref_r = ref.view(V, F, world, lay["streams"], P, 4).permute(2, 0, 1, 3, 4, 5)
+    got = allr.view(world, V, F, lay["streams"], P, 4)
+    equal = bool(torch.equal(ref_r, got))
+    h = lambda t: hashlib.sha256(t.contiguous().cpu().numpy().tobytes()).hexdigest()[:16]
+    out = {"equal": equal, "steps": V, "streams": nv, "records": int(got.numel() // 4),
+           "sha256_gathered": h(got), "sha256_single_process": h(ref_r),
+           "tracked_records": int((got[..., 2] == 0).sum().item()),
+           "seconds": time.perf_counter() - t0}
+    del ref_fe, st
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_variants(fe, sched, args, wl, F, C, reps=20):
@@ -588,14 +711,14 @@ def run_e2e(fe, ring, sched, args, dev, F, C):
     import torch
 
     from paper_2506_04359_b200.frontend import HostStream
-    B, H, pitch = F * C, ring.shape[2], ring.shape[3]
+    B, H, pitch, R = F * C, ring.shape[2], ring.shape[3], ring.shape[1]
     n_host = 4
-    # pinned host frames: n_host steps worth, batch order f*C + c
+    # pinned host frames: n_host steps worth of the rank's streams, batch order f*C + v
     host = torch.empty((n_host, B, H, pitch), dtype=torch.uint8, pin_memory=True)
     for s in range(n_host):
         for f in range(F):
-            for c in range(C):
-                host[s, f * C + c].copy_(ring[c, (s * F + f) % ring.shape[1]])
+            for v in range(C):
+                host[s, f * C + v].copy_(ring[sched.cams[v], (sched.phases[v] + s * F + f) % R])
     hs = HostStream(fe)
 
     def step(s):

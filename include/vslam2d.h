@@ -132,15 +132,23 @@ int v2d_detect_gftt(const uint8_t* const* l0_ptrs, int64_t l0_pitch, int B, int 
  *   ncc        nullable [B][P] fp32 last evaluated NCC (0 if none)
  *   iters_out  nullable [B][P] int32 work counters: bits 0..23 = Gauss-Newton
  *              steps over all levels, bits 24..31 = levels whose template was built
+ *   track_list nullable [B][P][4] fp32, 16-B aligned: the track-list record
+ *              (x, y, status, ncc) = (out_pos, (float)status, ncc) of every slot,
+ *              the unit the rig-wide all-gather ships ("we collect
+ *              all the available observations"), written by the same kernel
  * min_eig is in (gray/px)^2 per window pixel: lost at L0 when lambda_min(G)/n
- * < min_eig; coarse levels are skipped instead (reading #15).
- * flags: 0 or V2D_KLT_NCC_EACH_STEP; unknown bits -> V2D_EINVAL. */
+ * < min_eig; coarse levels are skipped instead (reading #15).  min_eig must be
+ * > 0 (reading #27: it guarantees det(G) > 0 for the closed-form 2x2 solve).
+ * flags: 0 or V2D_KLT_NCC_EACH_STEP; unknown bits -> V2D_EINVAL.
+ * V2D_EINVAL also for B*P > INT32_MAX (one warp per slot) and min_eig <= 0 / NaN;
+ * V2D_EALIGN for a track_list that is not 16-B aligned. */
 int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_pyr_ptrs,
                   const uint8_t* const* next_l0_ptrs, const float* const* next_pyr_ptrs,
                   int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                   const float* guess, const uint8_t* in_status, int P, int win, int iters,
                   float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
-                  float* ncc, int32_t* iters_out, unsigned flags, v2d_stream_t stream);
+                  float* ncc, int32_t* iters_out, float* track_list, unsigned flags,
+                  v2d_stream_t stream);
 
 /* Per-level patch features (variant f4; "a list of 9x9 image
  * patches taken from each level of the image pyramid").  For
@@ -150,7 +158,7 @@ int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_p
  * l0_ptrs[b] and levels >= 1 pyr_ptrs[b].
  *   pts   [B][P][2] fp32 L0 px; empty slots (-1,-1) / non-finite -> all-zero patches
  *   out   [B][P][levels][patch][patch] fp32
- * V2D_EINVAL: patch even, < 1 or > 31; bad levels / sizes. */
+ * V2D_EINVAL: patch even, < 1 or > 31; bad levels / sizes; B*P > INT32_MAX. */
 int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs,
                         int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                         int P, int patch, float* out, v2d_stream_t stream);

@@ -331,6 +331,11 @@ int v2dref_track_klt(const double* prev_pyr, const double* next_pyr,
   if (!prev_pyr || !next_pyr || (P > 0 && (!pts || !out_pos || !status))) return V2DREF_EINVAL;
   if (v2dref_level_dims(W, H, levels, Ws, Hs) != V2DREF_OK) return V2DREF_EINVAL;
   if (win < 3 || (win % 2) == 0 || iters < 1 || P < 0) return V2DREF_EINVAL;
+  /* reading #27: min_eig must be > 0.  The closed-form step eta = G^-1 b
+   * divides by det(G); lambda_min/n >= min_eig > 0 is what guarantees det > 0
+   * (D7 applies the conditioning test before any solve), so a non-positive
+   * threshold would let a rank-deficient window reach the division. */
+  if (!(min_eig > 0.0)) return V2DREF_EINVAL;
   const int r = (win - 1) / 2, n = win * win;
 
   /* Level planes and template-gradient planes Gx_L, Gy_L of the previous

@@ -41,7 +41,7 @@ int grid_k(int gx, int gy, int k, int K_min, int* k_out) {
 
 extern "C" {
 
-int v2d_version(void) { return 100; }
+int v2d_version(void) { return 200; }
 
 const char* v2d_strerror(int code) {
   switch (code) {
@@ -114,21 +114,24 @@ int v2d_track_klt(const uint8_t* const* prev_l0_ptrs, const float* const* prev_p
                   int64_t l0_pitch, int B, int W, int H, int levels, const float* pts,
                   const float* guess, const uint8_t* in_status, int P, int win, int iters,
                   float eps, float ncc_min, float min_eig, float* out_pos, uint8_t* status,
-                  float* ncc, int32_t* iters_out, unsigned flags, v2d_stream_t stream) {
+                  float* ncc, int32_t* iters_out, float* track_list, unsigned flags,
+                  v2d_stream_t stream) {
   v2d::Levels lv;
   if (flags & ~V2D_KLT_NCC_EACH_STEP) return V2D_EINVAL;
   if (B < 0 || P < 0) return V2D_EINVAL;
-  if ((int64_t)B * P > ((int64_t)1 << 40)) return V2D_EINVAL;
+  if ((int64_t)B * P > INT32_MAX) return V2D_EINVAL;  // one warp-CTA per slot: grid.x limit
+  if (track_list && (reinterpret_cast<uintptr_t>(track_list) & 15)) return V2D_EALIGN;
   if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
   if (win < 3 || win > V2D_MAX_WIN || (win % 2) == 0 || iters < 1) return V2D_EINVAL;
-  if (!(eps >= 0.0f) || std::isnan(ncc_min) || std::isnan(min_eig)) return V2D_EINVAL;
+  // min_eig > 0 (DESIGN reading #27): it is what guarantees det(G) > 0 for the 2x2 solve
+  if (!(eps >= 0.0f) || std::isnan(ncc_min) || !(min_eig > 0.0f)) return V2D_EINVAL;
   if ((int64_t)B * P > 0 && (!prev_l0_ptrs || !next_l0_ptrs || !pts || !out_pos || !status))
     return V2D_EINVAL;
   if ((int64_t)B * P > 0 && levels > 1 && (!prev_pyr_ptrs || !next_pyr_ptrs)) return V2D_EINVAL;
   if (l0_pitch < W || (l0_pitch % 16) != 0) return V2D_EALIGN;
   v2d::KltArgs a{W, H, P, win, iters, eps, ncc_min, min_eig, l0_pitch, flags};
   return v2d::launch_klt(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, B, lv, a, pts,
-                         guess, in_status, out_pos, status, ncc, iters_out,
+                         guess, in_status, out_pos, status, ncc, iters_out, track_list,
                          reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -137,6 +140,7 @@ int v2d_extract_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_p
                         int P, int patch, float* out, v2d_stream_t stream) {
   v2d::Levels lv;
   if (B < 0 || P < 0 || patch < 1 || patch > 31 || (patch % 2) == 0) return V2D_EINVAL;
+  if ((int64_t)B * P > INT32_MAX) return V2D_EINVAL;  // one warp per keypoint: grid.x limit
   if (make_levels(W, H, levels, &lv, nullptr)) return V2D_EINVAL;
   if ((int64_t)B * P > 0 && (!l0_ptrs || !pts || !out || (levels > 1 && !pyr_ptrs)))
     return V2D_EINVAL;

@@ -640,7 +640,7 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
            int B, Levels lv, KltArgs a, const float* __restrict__ pts,
            const float* __restrict__ guess, const uint8_t* __restrict__ in_status,
            float* __restrict__ out_pos, uint8_t* __restrict__ status, float* __restrict__ ncc,
-           int32_t* __restrict__ iters_out) {
+           int32_t* __restrict__ iters_out, float4* __restrict__ track_list) {
   extern __shared__ __align__(16) float s_mem[];  // kWarps * Smem<WIN>::TOTAL floats
   const int64_t warp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -696,6 +696,8 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
     status[warp] = (uint8_t)o.status;
     if (ncc) ncc[warp] = o.ncc;
     if (iters_out) iters_out[warp] = o.steps | (o.levels << 24);
+    // a7 track-list record (x, y, status, ncc): the rig-wide all-gather ships these
+    if (track_list) track_list[warp] = make_float4(ox, oy, (float)o.status, o.ncc);
   }
 }
 
@@ -704,26 +706,22 @@ void launch_win(const uint8_t* const* prev_l0, const float* const* prev_pyr,
                 const uint8_t* const* next_l0, const float* const* next_pyr, int B,
                 const Levels& lv, const KltArgs& a, const float* pts, const float* guess,
                 const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
-                int32_t* iters_out, cudaStream_t st) {
-  const int64_t warps = (int64_t)B * a.P;
+                int32_t* iters_out, float4* track_list, cudaStream_t st) {
+  const int64_t warps = (int64_t)B * a.P;  // <= INT32_MAX (checked by the ABI)
   const unsigned blocks = (unsigned)((warps + kWarps - 1) / kWarps);
   constexpr int smem = kWarps * Smem<WIN>::TOTAL * (int)sizeof(float);
-  static bool attr = false;  // opt in above 48 KB once per instantiation
-  if (!attr) {
-    cudaFuncSetAttribute(klt_kernel<WIN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    cudaFuncSetAttribute(klt_kernel<WIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    attr = true;
-  }
+  // below the 48 KB default for every window: no opt-in attribute, no per-process state
+  static_assert(smem <= 48 * 1024, "KLT tile exceeds the default dynamic smem limit");
   if (a.flags & V2D_KLT_NCC_EACH_STEP)
     klt_kernel<WIN, true><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr,
                                                           B, lv, a, pts, guess, in_status,
-                                                          out_pos, status, ncc, iters_out);
+                                                          out_pos, status, ncc, iters_out,
+                                                          track_list);
   else
     klt_kernel<WIN, false><<<blocks, kThreads, smem, st>>>(prev_l0, prev_pyr, next_l0, next_pyr,
                                                            B, lv, a, pts, guess, in_status,
-                                                           out_pos, status, ncc, iters_out);
+                                                           out_pos, status, ncc, iters_out,
+                                                           track_list);
 }
 
 }  // namespace
@@ -732,12 +730,12 @@ int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
                const uint8_t* const* next_l0, const float* const* next_pyr, int B,
                const Levels& lv, const KltArgs& a, const float* pts, const float* guess,
                const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
-               int32_t* iters_out, cudaStream_t st) {
+               int32_t* iters_out, float* track_list, cudaStream_t st) {
   if (B == 0 || a.P == 0) return V2D_OK;
 #define V2D_WIN_CASE(w)                                                                   \
   case w:                                                                                 \
     launch_win<w>(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a, pts, guess, in_status, \
-                  out_pos, status, ncc, iters_out, st);                                   \
+                  out_pos, status, ncc, iters_out, reinterpret_cast<float4*>(track_list), st); \
     break;
   switch (a.win) {
     V2D_WIN_CASE(3)

@@ -49,27 +49,30 @@ class Frontend2D:
         # K2 workspace (dense two-pass detection): B*H*W floats
         self.ws = torch.empty((self.B, cfg.H, v2d.workspace_pitch(cfg.W)), dtype=torch.float32,
                               device=d)
-        # pyramid pointer tables per parity: current and previous images
+        # pyramid pointer tables per parity: current and previous images (host
+        # arithmetic, one H2D copy each)
+        stride = self.pyr.stride(1) * 4
+        addr = [[self.pyr[par].data_ptr() + i * stride for i in range(self.B)] for par in (0, 1)]
         cur, prev = [], []
         for par in (0, 1):
-            base = v2d.ptrs_of(self.pyr[par])
-            other = v2d.ptrs_of(self.pyr[1 - par])
-            cur.append(base)
-            pv = torch.empty_like(base)
-            pv[cams:] = base[:-cams]          # frame f-1 of this step
-            pv[:cams] = other[-cams:]         # last frame of the previous step
-            prev.append(pv)
+            # frame f-1 of this step; for f = 0, the last frame of the previous step
+            pv = addr[1 - par][-cams:] + addr[par][:-cams]
+            cur.append(v2d.ptr_table(addr[par], d))
+            prev.append(v2d.ptr_table(pv, d))
         self.pyr_ptrs, self.prev_pyr_ptrs = cur, prev
         # our kernels per step: pyramid, GFTT pass A + pass B (workspace path), KLT
         self.launches_per_step = 4
 
     # ------------------------------------------------------------------
     def step(self, l0_ptrs: torch.Tensor, prev_l0_ptrs: torch.Tensor, parity: int,
-             status_out: torch.Tensor | None = None, events=None):
+             status_out: torch.Tensor | None = None, events=None,
+             track_list: torch.Tensor | None = None):
         """Enqueue one step.  l0_ptrs / prev_l0_ptrs: device int64 [B] pointer
         tables of frames t+f and t+f-1 (batch order f*C + c).  `events`
         (optional, 4 CUDA events) bracket the three launches for per-kernel
-        timing on the launching stream."""
+        timing on the launching stream.  `track_list` (optional fp32 [B, P, 4])
+        receives the step's (x, y, status, ncc) records from the KLT kernel
+        (SURVEY §8(a) a7)."""
         c, B = self.cfg, self.B
         W, H, L = c.W, c.H, c.levels
         if events is not None:
@@ -86,7 +89,7 @@ class Frontend2D:
         v2d.track_klt_ptrs(prev_l0_ptrs, self.prev_pyr_ptrs[parity], l0_ptrs,
                            self.pyr_ptrs[parity], self.pitch, B, W, H, L, self.kp_xy[:-1],
                            None, None, self.P, c.win, c.iters, c.eps, c.ncc_min, c.min_eig,
-                           self.pos, st, self.ncc, self.iters, c.klt_flags)
+                           self.pos, st, self.ncc, self.iters, c.klt_flags, track_list)
         if events is not None:
             events[3].record()
         self.kp_xy[0].copy_(self.kp_xy[-1], non_blocking=True)
@@ -123,13 +126,12 @@ class HostStream:
         B, C, P, F = fe.B, fe.C, fe.P, fe.F
         d = fe.dev
         self.dbuf = torch.empty((3, B, fe.cfg.H, fe.pitch), dtype=torch.uint8, device=d)
-        self.cur_t = [v2d.ptrs_of(self.dbuf[i]) for i in range(3)]
-        self.prev_t = []
-        for i in range(3):
-            pv = torch.empty_like(self.cur_t[i])
-            pv[C:] = self.cur_t[i][:-C]
-            pv[:C] = self.cur_t[(i - 1) % 3][-C:]
-            self.prev_t.append(pv)
+        stride = self.dbuf.stride(1)
+        addr = [[self.dbuf[i].data_ptr() + b * stride for b in range(B)] for i in range(3)]
+        self.cur_t = [v2d.ptr_table(addr[i], d) for i in range(3)]
+        # previous frame of batch entry f*C + c: entry (f-1)*C + c, or for f = 0 the
+        # last frame of the slot before
+        self.prev_t = [v2d.ptr_table(addr[(i - 1) % 3][-C:] + addr[i][:-C], d) for i in range(3)]
         self.copy = torch.cuda.Stream(device=d)
         self.ev_in = [torch.cuda.Event() for _ in range(3)]
         self.ev_done = [torch.cuda.Event() for _ in range(3)]
@@ -201,25 +203,37 @@ class HostStream:
 class RingSchedule:
     """Pointer tables for stepping through a device ring frames[C, R, H, pitch]
     F frames at a time (R must be a multiple of 2F so parity and ring index
-    advance together)."""
+    advance together).
 
-    def __init__(self, frames: torch.Tensor, F: int):
-        C, R = frames.shape[0], frames.shape[1]
+    `cams` / `phases` (optional, one entry per processed stream v) select the
+    ring camera of stream v and the ring frame it starts at: step s, frame f of
+    stream v is ring frame (phases[v] + s*F + f) mod R of camera cams[v] (batch
+    entry f*V + v), and `before_first[v]` is the frame before its start.  The
+    multi-GPU shards (shard.rig_shard) are such streams: a block of cameras at
+    phase 0, or one camera's frame chunk starting at its phase."""
+
+    def __init__(self, frames: torch.Tensor, F: int, cams=None, phases=None):
+        Cr, R = frames.shape[0], frames.shape[1]
         assert R % (2 * F) == 0, "ring length must be a multiple of 2F"
+        cams = list(range(Cr)) if cams is None else [int(c) for c in cams]
+        phases = [0] * len(cams) if phases is None else [int(p) for p in phases]
+        assert len(phases) == len(cams) and all(0 <= c < Cr for c in cams)
+        C = len(cams)
         self.C, self.R, self.F = C, R, F
+        self.cams, self.phases = cams, phases
         self.n_steps = R // F
         img = frames.stride(1) * frames.element_size()
         cam = frames.stride(0) * frames.element_size()
         base = frames.data_ptr()
         dev = frames.device
-        s = torch.arange(self.n_steps, device=dev, dtype=torch.int64)[:, None, None]
-        f = torch.arange(F, device=dev, dtype=torch.int64)[None, :, None]
-        c = torch.arange(C, device=dev, dtype=torch.int64)[None, None, :]
-        t = s * F + f
-        self.cur = (base + c * cam + (t % R) * img).reshape(self.n_steps, F * C).contiguous()
-        self.prev = (base + c * cam + ((t - 1) % R) * img).reshape(self.n_steps, F * C).contiguous()
-        last = (base + torch.arange(C, device=dev, dtype=torch.int64) * cam + (R - 1) * img)
-        self.before_first = last.contiguous()
+        addr = lambda v, t: base + cams[v] * cam + ((phases[v] + t) % R) * img
+        cur = [[addr(v, s * F + f) for f in range(F) for v in range(C)]
+               for s in range(self.n_steps)]
+        prev = [[addr(v, s * F + f - 1) for f in range(F) for v in range(C)]
+                for s in range(self.n_steps)]
+        self.cur = torch.tensor(cur, dtype=torch.int64).to(dev)      # [n_steps, F*C]
+        self.prev = torch.tensor(prev, dtype=torch.int64).to(dev)
+        self.before_first = v2d.ptr_table([addr(v, -1) for v in range(C)], dev)
 
     def tables(self, step: int):
         i = step % self.n_steps
@@ -304,9 +318,9 @@ class KeyframeTracker:
                            self.ncc, self.iters, c.klt_flags)
         v2d.track_survival(self.status[j], self.kf_member, self.counts)
         if self.group is not None:
-            import torch.distributed as dist
+            from .shard import all_reduce_sum_
             v2d.keyframe_decide(self.counts, self.T, self.flag, self.totals)
-            dist.all_reduce(self.totals, group=self.group)  # rig-wide Eq. 5 (NCCL)
+            all_reduce_sum_(self.totals, self.group)  # rig-wide Eq. 5 (NCCL)
             red = self.totals.to(torch.int32).view(1, 2)
             v2d.keyframe_decide(red, self.T, self.flag)
         else:

@@ -62,7 +62,7 @@ def load() -> ctypes.CDLL:
     L.v2d_keyframe_decide.argtypes = [vp, i, f, vp, vp, vp]
     L.v2d_refill_tracks.argtypes = [vp, vp, i, i, i, vp, i, i, vp, vp, vp, vp, vp, vp]
     L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
-                                vp, vp, vp, vp, ctypes.c_uint, vp]
+                                vp, vp, vp, vp, vp, ctypes.c_uint, vp]
     L.v2d_extract_patches.argtypes = [vp, vp, i64, i, i, i, i, vp, i, i, vp, vp]
     L.v2d_strerror.argtypes = [i]
     L.v2d_strerror.restype = ctypes.c_char_p
@@ -110,12 +110,19 @@ def grid_k(grid_x: int, grid_y: int, k: int, K_min: int) -> int:
     return out.value
 
 
+def ptr_table(addrs, device) -> torch.Tensor:
+    """Device int64 array holding the given byte addresses (host arithmetic, one
+    H2D copy: no kernel launches)."""
+    host = torch.tensor([int(a) for a in addrs], dtype=torch.int64)
+    return host.to(device)
+
+
 def ptrs_of(t: torch.Tensor) -> torch.Tensor:
     """Device int64 array of per-image base pointers of a batched tensor
-    t[B, ...] (no host sync: computed on the device)."""
-    B = t.shape[0]
+    t[B, ...] (addresses computed on the host, one H2D copy, no kernels)."""
     stride = t.stride(0) * t.element_size()
-    return t.data_ptr() + torch.arange(B, device=t.device, dtype=torch.int64) * stride
+    base = t.data_ptr()
+    return ptr_table((base + i * stride for i in range(t.shape[0])), t.device)
 
 
 def level_view(pyr: torch.Tensor, lay: Layout, L: int) -> torch.Tensor:
@@ -151,13 +158,13 @@ def detect_gftt_ptrs(l0_ptrs, l0_pitch, B, W, H, grid_x, grid_y, k, K_min, min_s
 
 def track_klt_ptrs(prev_l0_ptrs, prev_pyr_ptrs, next_l0_ptrs, next_pyr_ptrs, l0_pitch, B, W, H,
                    levels, pts, guess, in_status, P, win, iters, eps, ncc_min, min_eig, out_pos,
-                   status, ncc=None, iters_out=None, flags=0):
-    _need_cuda(pts, guess, in_status, out_pos, status, ncc, iters_out)
+                   status, ncc=None, iters_out=None, flags=0, track_list=None):
+    _need_cuda(pts, guess, in_status, out_pos, status, ncc, iters_out, track_list)
     _check(load().v2d_track_klt(_p(prev_l0_ptrs), _p(prev_pyr_ptrs), _p(next_l0_ptrs),
                                 _p(next_pyr_ptrs), l0_pitch, B, W, H, levels, _p(pts), _p(guess),
                                 _p(in_status), P, win, iters, float(eps), float(ncc_min),
                                 float(min_eig), _p(out_pos), _p(status), _p(ncc), _p(iters_out),
-                                int(flags), _stream()), "track_klt")
+                                _p(track_list), int(flags), _stream()), "track_klt")
 
 
 # --------------------------------------------------------------------------
@@ -205,8 +212,10 @@ def detect_gftt(frames: torch.Tensor, W: int, grid_x: int, grid_y: int, k: int =
 
 def track_klt(prev_frames, prev_pyr, next_frames, next_pyr, W: int, levels: int,
               pts: torch.Tensor, guess=None, in_status=None, win: int = 21, iters: int = 10,
-              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01, flags: int = 0):
-    """pts [B, P, 2] -> (pos [B,P,2], status u8 [B,P], ncc [B,P], iters int32 [B,P])."""
+              eps: float = 0.01, ncc_min: float = 0.8, min_eig: float = 0.01, flags: int = 0,
+              track_list: torch.Tensor | None = None):
+    """pts [B, P, 2] -> (pos [B,P,2], status u8 [B,P], ncc [B,P], iters int32 [B,P]);
+    track_list (optional fp32 [B,P,4]) also receives the (x, y, status, ncc) records."""
     B, H, pitch = _frames(prev_frames)
     _frames(next_frames)
     P = pts.shape[1]
@@ -220,7 +229,7 @@ def track_klt(prev_frames, prev_pyr, next_frames, next_pyr, W: int, levels: int,
                    ptrs_of(next_pyr), pitch, B, W, H, levels, pts,
                    None if guess is None else guess.contiguous().float(),
                    None if in_status is None else in_status.contiguous(), P, win, iters, eps,
-                   ncc_min, min_eig, pos, st, nc, it, flags)
+                   ncc_min, min_eig, pos, st, nc, it, flags, track_list)
     return pos, st, nc, it
 
 

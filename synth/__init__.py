@@ -205,12 +205,14 @@ class Stream:
 
 
 def make_stream(wl: Workload, ring: int, device="cpu", cams: list[int] | None = None,
-                 rank_salt: int = 0, smooth: bool = False) -> Stream:
+                 rank_salt: int = 0, smooth: bool = False, only=None) -> Stream:
     """Render `ring` frames for each camera in `cams` (default all).  Cameras
     (2i, 2i+1) form rectified stereo pairs when wl.stereo_disparity > 0: the
     right camera renders the left camera's texture and trajectory shifted by the
     disparity (a fronto-parallel plane), so cross-camera tracking (f2) has a
-    known answer; all other cameras are independent."""
+    known answer; all other cameras are independent.  `only` (optional, a set of
+    ring frame indices) renders just those frames of the same ring (the others
+    stay zero): a camera's frame t depends only on (seed, camera, ring, t)."""
     cams = list(range(wl.cams)) if cams is None else cams
     frames = torch.zeros((len(cams), ring, wl.H, wl.pitch), dtype=torch.uint8, device=device)
     offs = np.zeros((len(cams), ring, 2))
@@ -233,7 +235,12 @@ def make_stream(wl: Workload, ring: int, device="cpu", cams: list[int] | None = 
                                           smooth=smooth)
         tex = tex_cache[src]
         oo = o - np.array([disp, 0.0]) if stereo_right else o
-        render(tex, oo, wl.H, wl.W, wl.pitch, origin=(span_x, span_y), out=frames[ci])
+        if only is None:
+            render(tex, oo, wl.H, wl.W, wl.pitch, origin=(span_x, span_y), out=frames[ci])
+        else:
+            for t in sorted({int(t) % ring for t in only}):
+                render(tex, oo[t:t + 1], wl.H, wl.W, wl.pitch, origin=(span_x, span_y),
+                       out=frames[ci, t:t + 1])
         offs[ci] = oo
     return Stream(frames, offs, wl)
 

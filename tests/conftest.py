@@ -21,3 +21,14 @@ def pytest_configure(config):
 def cuda_available():
     import torch
     return torch.cuda.is_available()
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Print the session's KLT parity totals (oracle/parity.py SESSION) so a
+    test log carries total and attributable status flips."""
+    try:
+        from oracle import parity
+    except Exception:  # pragma: no cover - oracle not importable
+        return
+    if parity.SESSION["calls"]:
+        terminalreporter.write_line(parity.session_summary())

@@ -88,17 +88,26 @@ def test_validation_without_gpu(v2d):
     args = dict(eps=0.01, ncc=0.8, eig=0.01)
     f = ctypes.c_float
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 20, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, 0, N) == -1
+                           f(0.01), N, N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 31, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, 0, N) == -1
+                           f(0.01), N, N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 21, 0, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, 0, N) == -1
+                           f(0.01), N, N, N, N, N, 0, N) == -1
     assert L.v2d_track_klt(N, N, N, N, 72, 0, 70, 64, 3, N, N, N, 0, 21, 10, f(0.01), f(0.8),
-                           f(0.01), N, N, N, N, 0, N) == -2
+                           f(0.01), N, N, N, N, N, 0, N) == -2
+    # min_eig <= 0 or NaN (reading #27), B*P beyond the grid limit, unaligned track_list
+    for me in (0.0, -1.0, float("nan")):
+        assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 21, 10, f(0.01),
+                               f(0.8), f(me), N, N, N, N, N, 0, N) == -1
+    assert L.v2d_track_klt(N, N, N, N, 64, 65536, 64, 64, 3, N, N, N, 65536, 21, 10, f(0.01),
+                           f(0.8), f(0.01), N, N, N, N, N, 0, N) == -1
+    assert L.v2d_track_klt(N, N, N, N, 64, 0, 64, 64, 3, N, N, N, 0, 21, 10, f(0.01), f(0.8),
+                           f(0.01), N, N, N, N, ctypes.c_void_p(8), 0, N) == -2
+    assert L.v2d_extract_patches(N, N, 64, 65536, 64, 64, 3, N, 65536, 9, N, N) == -1
     # empty batches are valid no-ops (no CUDA call is made for B == 0)
     assert L.v2d_build_pyramid(N, 64, 0, 64, 64, 3, N, N) == 0
     assert L.v2d_strerror(-2).decode().startswith("pitch")
-    assert L.v2d_version() == 100
+    assert L.v2d_version() == 200
     del args
 
 

@@ -9,7 +9,7 @@ import torch
 
 import oracle
 import synth
-from oracle.parity import compare_klt
+from oracle.parity import POS_TOL, compare_klt
 
 pytestmark = pytest.mark.gpu
 
@@ -79,6 +79,8 @@ def test_fullsize_sampled_parity(name):
         gpos = fe.pos[b].cpu().numpy()[pick]
         gst = fe.status[b].cpu().numpy()[pick]
         stats = compare_klt(pts_all[pick], gpos, gst, opos, ost, dg)
+        assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
+        assert stats["flips_unattributable"] == 0, stats
         assert stats["both_tracked"] > 0.5 * len(pick), stats
 
 
@@ -142,4 +144,6 @@ def test_multistep_stream_parity_c2():
                                               ncc_min=wl.ncc_min, min_eig=wl.min_eig)
         stats = compare_klt(pts[pick], fe.pos[b].cpu().numpy()[pick],
                             fe.status[b].cpu().numpy()[pick], opos, ost, dg)
+        assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
+        assert stats["flips_unattributable"] == 0, stats
         assert stats["both_tracked"] > 0.5 * len(pick), (s, stats)

@@ -10,7 +10,7 @@ import torch
 
 import oracle
 import synth
-from oracle.parity import compare_klt
+from oracle.parity import POS_TOL, compare_klt
 
 pytestmark = pytest.mark.gpu
 
@@ -73,4 +73,6 @@ def test_fuzz_detect_and_track(case):
         _, d0 = oracle.build_pyramid(prev[b], levels)
         _, d1 = oracle.build_pyramid(nxt[b], levels)
         opos, ost, onc, dg = oracle.track_klt(d0, d1, W, H, levels, pts[b], win=win)
-        compare_klt(pts[b], pos[b].cpu().numpy(), status[b].cpu().numpy(), opos, ost, dg)
+        stats = compare_klt(pts[b], pos[b].cpu().numpy(), status[b].cpu().numpy(), opos, ost, dg)
+        assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
+        assert stats["flips_unattributable"] == 0, stats

@@ -9,7 +9,7 @@ import torch
 
 import oracle
 import synth
-from oracle.parity import compare_klt, gpu_level_planes
+from oracle.parity import POS_TOL, compare_klt, gpu_level_planes
 
 pytestmark = pytest.mark.gpu
 
@@ -159,6 +159,15 @@ def test_detect_rejects_bad_k():
 
 
 # ---------------------------------------------------------------------- KLT
+def _strict(stats):
+    """The KLT bar, asserted explicitly in every KLT test (compare_klt also
+    raises): no position of a slot tracked on both sides off by more than
+    0.01 px, no status flip outside its own decision's band."""
+    assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
+    assert stats["flips_unattributable"] == 0, stats
+    return stats
+
+
 def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in_status=None,
               eps=0.01, each_step=False):
     B = fr_prev.shape[0]
@@ -181,7 +190,7 @@ def _klt_case(fr_prev, fr_next, W, levels, pts, win=21, iters=10, guess=None, in
             d0, d1, W, H, levels, pts[b], guess=None if guess is None else guess[b],
             in_status=None if in_status is None else in_status[b], win=win, iters=iters, eps=eps,
             ncc_each_step=each_step)
-        stats.append(compare_klt(pts[b], pos[b], st[b], opos, ost, dg))
+        stats.append(_strict(compare_klt(pts[b], pos[b], st[b], opos, ost, dg)))
     return stats
 
 
@@ -237,6 +246,48 @@ def test_klt_edge_cases():
     pos, st, nc, it = v2d.track_klt(d, p, d, p, W, 3, good)
     assert st.tolist() == [[0, 0]]
     assert torch.equal(pos, good)
+
+
+def test_klt_rank_deficient_window_and_min_eig_contract():
+    """Singular G (vertical stripes: Ty = 0, lambda_min = 0): LOST_SMALL_EIG on
+    both sides for any positive min_eig (reading #27); min_eig <= 0 is rejected
+    by the ABI (and by the oracle, tests/test_oracle_klt.py)."""
+    W, H = 160, 120
+    cols = (np.arange(W) * 37 % 251).astype(np.uint8)
+    f0 = np.ascontiguousarray(np.tile(cols, (H, 1)))[None]
+    pts = np.array([[[80, 60], [50.5, 40.25], [30, 90]]], np.float32)
+    for me in (0.01, 1e-30):
+        dp = _to_dev(f0)
+        pp = v2d.build_pyramid(dp, W, 2)
+        pos, st, nc, it = v2d.track_klt(dp, pp, dp, pp, W, 2, torch.from_numpy(pts).cuda(),
+                                        min_eig=me)
+        assert st.tolist() == [[v2d.LOST_SMALL_EIG] * 3]
+        _, d0 = oracle.build_pyramid(f0[0], 2)
+        opos, ost, onc, dg = oracle.track_klt(d0, d0, W, H, 2, pts[0], min_eig=me)
+        assert ost.tolist() == st[0].tolist()
+        _strict(compare_klt(pts[0], pos[0].cpu().numpy(), st[0].cpu().numpy(), opos, ost, dg))
+    for me in (0.0, -1.0):
+        with pytest.raises(v2d.V2DError):
+            v2d.track_klt(dp, pp, dp, pp, W, 2, torch.from_numpy(pts).cuda(), min_eig=me)
+
+
+def test_klt_track_list_records():
+    """The a7 track-list records written by the KLT kernel equal (pos, status,
+    ncc) of the same launch, bit for bit."""
+    W, H = 320, 240
+    fr, _ = _stream(W, H, 2, 21)
+    dp, dn = _to_dev(fr[:1]), _to_dev(fr[1:])
+    pp, pn = v2d.build_pyramid(dp, W, 3), v2d.build_pyramid(dn, W, 3)
+    pts = oracle.detect_gftt(fr[0], 4, 4, k=8, border=11)[0].reshape(1, -1, 2)
+    tp = torch.from_numpy(pts).cuda()
+    rec = torch.full((1, pts.shape[1], 4), 7.0, device="cuda")
+    pos, st, nc, it = v2d.track_klt(dp, pp, dn, pn, W, 3, tp, track_list=rec)
+    assert torch.equal(rec[..., :2], pos)
+    assert torch.equal(rec[..., 2], st.float())
+    assert torch.equal(rec[..., 3], nc)
+    with pytest.raises(v2d.V2DError):  # not 16-B aligned
+        raw = torch.zeros(4 * pts.shape[1] + 1, device="cuda")
+        v2d.track_klt(dp, pp, dn, pn, W, 3, tp, track_list=raw[1:].view(1, -1, 4))
 
 
 def test_klt_noise_rejects():
@@ -342,8 +393,8 @@ def test_keyframe_tracker_stepwise_parity():
             _, dc = oracle.build_pyramid(frames[c, t], levels)
             opos, ost, onc, dg = oracle.track_klt(dp, dc, W, H, levels, tr0[c], in_status=st0[c])
             keep = ~refilled[c]
-            compare_klt(tr0[c][keep], pre_tracks[c][keep], pre_status[c][keep], opos[keep],
-                        ost[keep], dg[keep])
+            _strict(compare_klt(tr0[c][keep], pre_tracks[c][keep], pre_status[c][keep],
+                                opos[keep], ost[keep], dg[keep]))
             counts_kf += int(kf0[c].sum())
             counts_sv += int((kf0[c].astype(bool) & (pre_status[c] == 0)).sum())
         assert flag == int(oracle.keyframe_due(counts_kf, counts_sv, T))

@@ -14,7 +14,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2506_04359_b200.shard import Shard, TrackGather, shard_plan
+from paper_2506_04359_b200.shard import (RECORD, TrackGather, all_streams, rig_shard,
+                                          shard_plan)
 
 
 def _free_port():
@@ -61,14 +62,15 @@ def _frames():
 
 
 def _track_unit(frames, cam, f):
-    """Oracle tracks for frame pair (f-1 -> f) of camera cam: (pos f32, status)."""
+    """Oracle track-list records for frame pair (f-1 -> f) of camera cam:
+    fp32 [P, 4] = (x, y, status, ncc)."""
     prev, cur = frames[cam, f - 1], frames[cam, f]
     _, dp = oracle.build_pyramid(prev, WL.levels)
     _, dc = oracle.build_pyramid(cur, WL.levels)
     xy, _, _ = oracle.detect_gftt(prev, WL.grid_x, WL.grid_y, k=WL.k, border=WL.border)
-    pos, st, _, _ = oracle.track_klt(dp, dc, WL.W, WL.H, WL.levels, xy.reshape(-1, 2),
-                                     win=WL.win)
-    return pos.astype(np.float32), st
+    pos, st, nc, _ = oracle.track_klt(dp, dc, WL.W, WL.H, WL.levels, xy.reshape(-1, 2),
+                                      win=WL.win)
+    return np.concatenate([pos, st[:, None], nc[:, None]], 1).astype(np.float32)
 
 
 def _worker(rank, world, port, q):
@@ -83,22 +85,19 @@ def _worker(rank, world, port, q):
         n_max = max(len(shard_plan(WL.cams, N_FRAMES, world, r).cams) *
                     (shard_plan(WL.cams, N_FRAMES, world, r).frame_end -
                      shard_plan(WL.cams, N_FRAMES, world, r).frame_begin) for r in range(world))
-        pos = torch.full((n_max, P, 2), -7.0)
-        st = torch.full((n_max, P), 255, dtype=torch.uint8)
+        recs = torch.full((n_max, P, RECORD), -7.0)
         for i, (c, f) in enumerate(units):
-            p, s = _track_unit(frames, c, f)
-            pos[i] = torch.from_numpy(p)
-            st[i] = torch.from_numpy(s)
+            recs[i] = torch.from_numpy(_track_unit(frames, c, f))
         tg = TrackGather(n_max, P, "cpu")
-        all_pos, all_st = tg.gather(pos, st)
+        tg.gather(recs)
         if rank == 0:
             out = {}
             for r in range(world):
                 shr = shard_plan(WL.cams, N_FRAMES, world, r)
                 ur = [(c, f) for f in range(shr.frame_begin, shr.frame_end) for c in shr.cams]
-                bp, bs = tg.rank_block(r)
+                br = tg.rank_block(r)
                 for i, u in enumerate(ur):
-                    out[u] = (bp[i].numpy().copy(), bs[i].numpy().copy())
+                    out[u] = br[i].numpy().copy()
             q.put(out)
     finally:
         dist.destroy_process_group()
@@ -118,14 +117,40 @@ def test_gloo_sharded_equals_single(world):
         assert p.exitcode == 0
     frames = _frames()
     assert set(out) == {(c, f) for c in range(WL.cams) for f in range(1, N_FRAMES)}
-    for (c, f), (pos, st) in out.items():
-        rp, rs = _track_unit(frames, c, f)
-        assert np.array_equal(pos, rp) and np.array_equal(st, rs)
+    for (c, f), rec in out.items():
+        assert np.array_equal(rec, _track_unit(frames, c, f))
 
 
 def test_track_gather_single_rank_identity():
     tg = TrackGather(3, 4, "cpu")
-    p = torch.randn(3, 4, 2)
-    s = torch.randint(0, 5, (3, 4), dtype=torch.uint8)
-    ap, as_ = tg.gather(p, s)
-    assert torch.equal(ap, p) and torch.equal(as_, s)
+    p = torch.randn(3, 4, RECORD)
+    assert torch.equal(tg.gather(p), p) and torch.equal(tg.rank_block(0), p)
+
+
+@pytest.mark.parametrize("C,G,R", [(32, 1, 6), (32, 2, 8), (32, 4, 8), (32, 8, 16), (8, 2, 8),
+                                   (8, 8, 8), (2, 1, 32), (2, 2, 32), (2, 4, 32), (2, 8, 32)])
+def test_rig_shard_covers_the_ring_once(C, G, R):
+    """The bench's streams: every (camera, ring frame) is tracked by exactly one
+    rank over one pass of the ring (R frames from each stream's phase for C >= G;
+    R*C/G frames of a chunk otherwise), camera blocks contiguous."""
+    per_stream = R if C >= G else R * C // G
+    seen = {}
+    for r in range(G):
+        sh = rig_shard(C, R, G, r)
+        assert len(sh.cams) == max(1, C // G)
+        assert list(sh.cams) == list(range(sh.cams[0], sh.cams[-1] + 1))
+        for c, ph in zip(sh.cams, sh.phases):
+            for t in range(per_stream):
+                u = (c, (ph + t) % R)
+                assert u not in seen
+                seen[u] = r
+    assert set(seen) == {(c, t) for c in range(C) for t in range(R)}
+    al = all_streams(C, R, G)
+    assert len(al.cams) == max(C, G)
+
+
+def test_rig_shard_rejects():
+    with pytest.raises(ValueError):
+        rig_shard(2, 31, 4, 0)  # ring not divisible into 2 chunks per camera
+    with pytest.raises(ValueError):
+        rig_shard(3, 30, 2, 0)

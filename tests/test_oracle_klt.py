@@ -158,6 +158,27 @@ def test_flat_region_small_eig():
     assert st[0] == oracle.LOST_SMALL_EIG and st[1] == oracle.TRACKED
 
 
+def test_rank_deficient_window_small_eig():
+    """Vertical stripes: Ty = 0 everywhere, so G = [[a, 0], [0, 0]] is singular
+    (lambda_min = 0 exactly).  With any positive min_eig (even 1e-30) the window
+    is LOST_SMALL_EIG at L0 and no closed-form solve divides by det = 0."""
+    cols = (np.arange(W) * 37 % 251).astype(np.uint8)
+    f0 = np.ascontiguousarray(np.tile(cols, (H, 1)))
+    pts = np.array([[160, 120], [100.5, 80.25]], np.float32)
+    for me in (0.01, 1e-30):
+        _, (pos, st, nc, dg) = _track(f0, f0, 2, pts=pts, min_eig=me)
+        assert list(st) == [oracle.LOST_SMALL_EIG] * 2
+        assert np.all(pos == -1)
+
+
+@pytest.mark.parametrize("me", [0.0, -0.5, float("nan")])
+def test_non_positive_min_eig_rejected(me):
+    """Reading #27: min_eig must be > 0 (it is what guarantees det(G) > 0)."""
+    f0 = np.full((H, W), 90, np.uint8)
+    with pytest.raises(Exception):
+        _track(f0, f0, 2, pts=np.array([[100, 100]], np.float32), min_eig=me)
+
+
 def test_leaving_image_is_oob():
     """A point whose true motion leaves the half-window margin is LOST_OOB."""
     f0, f1 = _int_shift(_big(5), 6, 0)
