@@ -99,13 +99,15 @@ def _host_staged(group) -> bool:
 
 
 def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
-    """dist.all_gather_into_tensor on the current stream (rank-major)."""
+    """dist.all_gather_into_tensor on the current stream (rank-major), on flat
+    views (out holds world * inp.numel() elements in rank order)."""
+    flat_out = out.view(-1)
     if inp.is_cuda and _host_staged(group):
-        h = torch.empty(out.shape, dtype=out.dtype)
-        dist.all_gather_into_tensor(h, inp.cpu(), group=group)
-        out.copy_(h, non_blocking=False)
+        h = torch.empty(flat_out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(h, inp.reshape(-1).cpu(), group=group)
+        flat_out.copy_(h, non_blocking=False)
     else:
-        dist.all_gather_into_tensor(out, inp.contiguous(), group=group)
+        dist.all_gather_into_tensor(flat_out, inp.contiguous().view(-1), group=group)
 
 
 def all_reduce_sum_(t: torch.Tensor, group=None):

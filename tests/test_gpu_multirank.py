@@ -25,6 +25,21 @@ pytestmark = pytest.mark.gpu
 STEPS = 3
 
 
+def _collect(procs, q, n):
+    """n queue items, failing fast if a rank process dies first."""
+    import queue
+    import time
+    out, t0 = [], time.time()
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"rank process failed: exit codes {dead}"
+            assert time.time() - t0 < 600, "rank processes timed out"
+    return out
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -99,7 +114,7 @@ def test_sharded_gather_equals_single_process(name, world, F):
              for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=600)
+    got = _collect(procs, q, 1)[0]
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -166,7 +181,7 @@ def test_keyframe_group_decision_equals_single_process():
              for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (f, t)) for r, f, t in (q.get(timeout=600) for _ in range(world)))
+    res = dict((r, (f, t)) for r, f, t in _collect(procs, q, world))
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
