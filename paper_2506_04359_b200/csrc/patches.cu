@@ -5,22 +5,27 @@
 // out[b][p][L][v][u] = S(I_L, c_L + (u - r, v - r)),  c_L = (p + 0.5)/2^L - 0.5,
 // bilinear with clamp-to-edge (D2), r = (patch-1)/2.
 //
-// B200 mapping: a gather on the resident pyramid — one warp per keypoint; per
-// level the (patch+1)^2 pixel block is staged once in shared memory (the
-// samples share their bilinear weights), then lanes form the patch x patch
-// samples and store the contiguous [levels][patch][patch] block coalesced.
+// B200 mapping: a gather on the resident pyramid — one warp per keypoint.
+// Every sample of one level shares the fractional offset of c_L, so a level's
+// patch is a fixed-weight bilinear of one (patch+1)^2 block of pixels.  The warp
+// first issues the loads of the blocks of ALL levels (up to kBudget pixels at a
+// time: 5 levels x 10 x 10 for 9x9 patches), independent clamped loads with
+// the whole batch in flight (the kernel is latency-bound: one level at a time
+// left ~4 dependent load rounds per level per warp), into shared memory; then
+// lanes form every sample of those levels with the same expression order as D2
+// and store the contiguous [levels][patch][patch] block coalesced.
 #include "common.cuh"
 
 namespace v2d {
 namespace {
 
 constexpr int kWarps = 8;
+constexpr int kBudget = 1024;  // staged pixels per warp (4 KB of shared memory)
 
-// Every sample of one level shares the fractional offset of c_L, so a level's
-// patch is a fixed-weight bilinear of one (patch+1)^2 block of pixels: the warp
-// stages that block (clamp-to-edge, row-coalesced loads) in shared memory once
-// and forms each sample from it with the same expression order as D2.
-constexpr int kTile = 32;  // max block edge (patch <= 31)
+__device__ __forceinline__ float level_px(const uint8_t* l0, const float* lvl, int64_t pitch, int x,
+                                          int y, int L) {
+  return L == 0 ? (float)__ldg(l0 + (int64_t)y * pitch + x) : __ldg(lvl + (int64_t)y * pitch + x);
+}
 
 template <int PATCH>  // compile-time patch edge: the index divisions become multiply-shifts
 __global__ void __launch_bounds__(32 * kWarps)
@@ -28,7 +33,9 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
                int64_t l0_pitch, int B, Levels lv, const float* __restrict__ pts, int P,
                float* __restrict__ out) {
   constexpr int patch = PATCH;
-  __shared__ float s_blk[kWarps][kTile * kTile];
+  constexpr int n = patch * patch, r = (patch - 1) / 2, e = patch + 1, EE = e * e;
+  constexpr int kPerBatch = kBudget / EE > 0 ? kBudget / EE : 1;  // levels staged at once
+  __shared__ float s_blk[kWarps][kPerBatch * EE];
   const int64_t kp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (kp >= (int64_t)B * P) return;  // warp-uniform
@@ -36,34 +43,42 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
   const int b = (int)(kp / P);
   const float px0 = pts[2 * kp], py0 = pts[2 * kp + 1];
   const bool empty = (px0 == -1.0f && py0 == -1.0f) || !isfinite(px0) || !isfinite(py0);
-  constexpr int n = patch * patch, r = (patch - 1) / 2, e = patch + 1;
   float* o = out + kp * (int64_t)lv.n * n;
   if (empty) {
     for (int i = lane; i < lv.n * n; i += 32) o[i] = 0.0f;
     return;
   }
-  for (int L = 0; L < lv.n; ++L) {
-    const float scale = __int_as_float((127 - L) << 23);  // 2^-L
-    const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
-    const float fx = floorf(cx), fy = floorf(cy);
-    const float wa = cx - fx, wb = cy - fy;
-    const int bx = (int)fx - r, by = (int)fy - r;  // block origin (pixel of sample u=v=0)
-    const int W = lv.W[L], H = lv.H[L];
+  const uint8_t* l0 = l0_ptrs[b];
+  const float* pyr = lv.n > 1 ? pyr_ptrs[b] : nullptr;
+  for (int L0 = 0; L0 < lv.n; L0 += kPerBatch) {
+    const int nb = min(kPerBatch, lv.n - L0);
     __syncwarp();
-    for (int j = lane; j < e * e; j += 32) {
-      const int rr = j / e, cc = j - rr * e;
-      const int x = min(max(bx + cc, 0), W - 1), y = min(max(by + rr, 0), H - 1);
-      blk[rr * kTile + cc] =
-          L == 0 ? (float)__ldg(l0_ptrs[b] + (int64_t)y * l0_pitch + x)
-                 : __ldg(pyr_ptrs[b] + lv.offset[L] + (int64_t)y * lv.pitch[L] + x);
+    // ---- stage the (patch+1)^2 blocks of levels L0 .. L0+nb-1 (clamp-to-edge)
+#pragma unroll 4
+    for (int j = lane; j < nb * EE; j += 32) {
+      const int q = j / EE, jj = j - q * EE;  // level L0+q, block element jj
+      const int L = L0 + q;
+      const int rr = jj / e, cc = jj - rr * e;
+      const float scale = __int_as_float((127 - L) << 23);  // 2^-L
+      const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
+      const int bx = (int)floorf(cx) - r, by = (int)floorf(cy) - r;  // block origin
+      const int x = min(max(bx + cc, 0), lv.W[L] - 1), y = min(max(by + rr, 0), lv.H[L] - 1);
+      blk[j] = level_px(l0, L ? pyr + lv.offset[L] : nullptr, L ? lv.pitch[L] : l0_pitch, x, y, L);
     }
     __syncwarp();
-    float* oL = o + L * n;
-    for (int i = lane; i < n; i += 32) {
-      const int v = i / patch, u = i - v * patch;
-      const float* q = blk + v * kTile + u;
-      const float top = fmaf(wa, q[1] - q[0], q[0]);
-      const float bot = fmaf(wa, q[kTile + 1] - q[kTile], q[kTile]);
+    // ---- samples of those levels, stored contiguously ([L][v][u])
+    float* oL = o + L0 * n;
+#pragma unroll 4
+    for (int i = lane; i < nb * n; i += 32) {
+      const int q = i / n, ii = i - q * n;
+      const int L = L0 + q;
+      const int v = ii / patch, u = ii - v * patch;
+      const float scale = __int_as_float((127 - L) << 23);
+      const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
+      const float wa = cx - floorf(cx), wb = cy - floorf(cy);
+      const float* t = blk + q * EE + v * e + u;
+      const float top = fmaf(wa, t[1] - t[0], t[0]);
+      const float bot = fmaf(wa, t[e + 1] - t[e], t[e]);
       oL[i] = fmaf(wb, bot - top, top);
     }
   }

@@ -287,6 +287,7 @@ class KeyframeTracker:
         self.totals = torch.zeros((2,), dtype=torch.int64, device=d)
         self.ncc = torch.zeros((C, P), device=d)
         self.iters = torch.zeros((C, P), dtype=torch.int32, device=d)
+        self.kf_count = torch.zeros((), dtype=torch.int64, device=d)  # keyframes so far
         self.cur = 0
 
     def _keyframe_branch(self, l0_ptrs, j):
@@ -347,6 +348,7 @@ class KeyframeTracker:
             self._l0.copy_(self._ft.index_select(0, torch.remainder(self._t, R)).view(-1))
             self._pl0.copy_(self._ft.index_select(0, torch.remainder(self._t - 1, R)).view(-1))
             self.step(self._l0, self._pl0)
+            self.kf_count.add_(self.flag[0])
             self._t.add_(1)
 
         torch.cuda.synchronize(self.dev)
