@@ -22,12 +22,7 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kBudget = 1024;  // staged pixels per warp (4 KB of shared memory)
 
-__device__ __forceinline__ float level_px(const uint8_t* l0, const float* lvl, int64_t pitch, int x,
-                                          int y, int L) {
-  return L == 0 ? (float)__ldg(l0 + (int64_t)y * pitch + x) : __ldg(lvl + (int64_t)y * pitch + x);
-}
-
-template <int PATCH>  // compile-time patch edge: the index divisions become multiply-shifts
+template <int PATCH>  // compile-time patch edge
 __global__ void __launch_bounds__(32 * kWarps)
 patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* __restrict__ pyr_ptrs,
                int64_t l0_pitch, int B, Levels lv, const float* __restrict__ pts, int P,
@@ -35,6 +30,7 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
   constexpr int patch = PATCH;
   constexpr int n = patch * patch, r = (patch - 1) / 2, e = patch + 1, EE = e * e;
   constexpr int kPerBatch = kBudget / EE > 0 ? kBudget / EE : 1;  // levels staged at once
+  constexpr int kLd = (EE + 31) / 32, kSm = (n + 31) / 32;         // per lane and level
   __shared__ float s_blk[kWarps][kPerBatch * EE];
   const int64_t kp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -48,38 +44,69 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
     for (int i = lane; i < lv.n * n; i += 32) o[i] = 0.0f;
     return;
   }
+  // this lane's block elements (row, col) and sample positions (v, u): the same at
+  // every level, so all index arithmetic is done once
+  int br[kLd], bc[kLd], sv[kSm], su[kSm];
+#pragma unroll
+  for (int m = 0; m < kLd; ++m) {
+    const int j = min(lane + 32 * m, EE - 1);
+    br[m] = j / e;
+    bc[m] = j - br[m] * e;
+  }
+#pragma unroll
+  for (int m = 0; m < kSm; ++m) {
+    const int i = min(lane + 32 * m, n - 1);
+    sv[m] = i / patch;
+    su[m] = i - sv[m] * patch;
+  }
   const uint8_t* l0 = l0_ptrs[b];
   const float* pyr = lv.n > 1 ? pyr_ptrs[b] : nullptr;
   for (int L0 = 0; L0 < lv.n; L0 += kPerBatch) {
     const int nb = min(kPerBatch, lv.n - L0);
     __syncwarp();
-    // ---- stage the (patch+1)^2 blocks of levels L0 .. L0+nb-1 (clamp-to-edge)
-#pragma unroll 4
-    for (int j = lane; j < nb * EE; j += 32) {
-      const int q = j / EE, jj = j - q * EE;  // level L0+q, block element jj
+    // ---- stage the (patch+1)^2 blocks of levels L0 .. L0+nb-1 (clamp-to-edge);
+    // every load of the batch is independent, so all of them are in flight
+    for (int q = 0; q < nb; ++q) {
       const int L = L0 + q;
-      const int rr = jj / e, cc = jj - rr * e;
       const float scale = __int_as_float((127 - L) << 23);  // 2^-L
       const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
       const int bx = (int)floorf(cx) - r, by = (int)floorf(cy) - r;  // block origin
-      const int x = min(max(bx + cc, 0), lv.W[L] - 1), y = min(max(by + rr, 0), lv.H[L] - 1);
-      blk[j] = level_px(l0, L ? pyr + lv.offset[L] : nullptr, L ? lv.pitch[L] : l0_pitch, x, y, L);
+      const int Wl = lv.W[L] - 1, Hl = lv.H[L] - 1;
+      float* dst = blk + q * EE;
+      if (L == 0) {
+#pragma unroll
+        for (int m = 0; m < kLd; ++m) {
+          const int x = min(max(bx + bc[m], 0), Wl), y = min(max(by + br[m], 0), Hl);
+          const float v = (float)__ldg(l0 + (int64_t)y * l0_pitch + x);
+          if (lane + 32 * m < EE) dst[lane + 32 * m] = v;
+        }
+      } else {
+        const float* pl = pyr + lv.offset[L];
+        const int64_t pitch = lv.pitch[L];
+#pragma unroll
+        for (int m = 0; m < kLd; ++m) {
+          const int x = min(max(bx + bc[m], 0), Wl), y = min(max(by + br[m], 0), Hl);
+          const float v = __ldg(pl + (int64_t)y * pitch + x);
+          if (lane + 32 * m < EE) dst[lane + 32 * m] = v;
+        }
+      }
     }
     __syncwarp();
     // ---- samples of those levels, stored contiguously ([L][v][u])
-    float* oL = o + L0 * n;
-#pragma unroll 4
-    for (int i = lane; i < nb * n; i += 32) {
-      const int q = i / n, ii = i - q * n;
+    for (int q = 0; q < nb; ++q) {
       const int L = L0 + q;
-      const int v = ii / patch, u = ii - v * patch;
       const float scale = __int_as_float((127 - L) << 23);
       const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
       const float wa = cx - floorf(cx), wb = cy - floorf(cy);
-      const float* t = blk + q * EE + v * e + u;
-      const float top = fmaf(wa, t[1] - t[0], t[0]);
-      const float bot = fmaf(wa, t[e + 1] - t[e], t[e]);
-      oL[i] = fmaf(wb, bot - top, top);
+      const float* src = blk + q * EE;
+      float* oL = o + L * n;
+#pragma unroll
+      for (int m = 0; m < kSm; ++m) {
+        const float* t = src + sv[m] * e + su[m];
+        const float top = fmaf(wa, t[1] - t[0], t[0]);
+        const float bot = fmaf(wa, t[e + 1] - t[e], t[e]);
+        if (lane + 32 * m < n) oL[lane + 32 * m] = fmaf(wb, bot - top, top);
+      }
     }
   }
 }

@@ -52,8 +52,12 @@ class Guarded:
     def check(self, what):
         torch.cuda.synchronize()
         g, n = self.g, self.n
-        assert torch.equal(self.raw[:g], self.ref[:g]), f"{what}: write before the buffer"
-        assert torch.equal(self.raw[g + n:], self.ref[g + n:]), f"{what}: write after the buffer"
+        # compare bytes (the float canary is a NaN, which never equals itself)
+        raw, ref = self.raw.view(torch.uint8), self.ref.view(torch.uint8)
+        esz = self.raw.element_size()
+        assert torch.equal(raw[:g * esz], ref[:g * esz]), f"{what}: write before the buffer"
+        assert torch.equal(raw[(g + n) * esz:], ref[(g + n) * esz:]), \
+            f"{what}: write after the buffer"
 
 
 def _frames(fr: np.ndarray, poison: bool, seed=0):
