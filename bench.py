@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--overlap", type=int, default=0,
+                    help="1: the first frame's KLT launch runs on a second stream, concurrent "
+                         "with the detection launch (Frontend2D overlap)")
     ap.add_argument("--extras", action="store_true",
                     help="also time the SURVEY §8(f) variants on the last step's data")
     return ap.parse_args()
@@ -330,14 +333,14 @@ def workload_config(wl, lay, n_gpus):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def make_frontend(wl, streams, F, dev):
+def make_frontend(wl, streams, F, dev, overlap=False):
     from paper_2506_04359_b200 import vslam2d as v2d
     from paper_2506_04359_b200.frontend import Frontend2D
     cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
                              grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
                              win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
                              min_eig=wl.min_eig)
-    return Frontend2D(cfg, streams, F, dev, wl.pitch)
+    return Frontend2D(cfg, streams, F, dev, wl.pitch, overlap=overlap)
 
 
 def render_streams(wl, R, shard, dev, only=None):
@@ -378,7 +381,7 @@ def main():
     lay = bench_layout(wl, world, args.frames_per_step)
     F, R, streams = lay["F"], lay["R"], lay["streams"]
     shard = rig_shard(C, R, world, rank)
-    fe = make_frontend(wl, streams, F, dev)
+    fe = make_frontend(wl, streams, F, dev, overlap=bool(args.overlap))
     B, P = fe.B, fe.P
 
     t_render = time.perf_counter()

@@ -23,9 +23,23 @@ from .vslam2d import FrontendConfig
 
 
 class Frontend2D:
+    """overlap=True: the KLT launch of the step's first frame (the C images whose
+    keypoints were detected in the previous step) runs on a second stream,
+    concurrently with the detection launch of this step — the two are
+    independent (K2(t) needs frame t only, K3(t) needs the pyramids of t-1 and t
+    and the keypoints of t-1), and their pipes are complementary (K2: integer alu
+    pipe; K3: fma pipe and shared-memory loads).  The frames f >= 1 of a step
+    (F > 1) are tracked after the detection launch, as before.  Results are
+    identical (same kernels, same inputs)."""
+
     def __init__(self, cfg: FrontendConfig, cams: int, frames_per_step: int, device,
-                 l0_pitch: int):
+                 l0_pitch: int, overlap: bool = False):
         self.cfg, self.C, self.F, self.dev = cfg, cams, frames_per_step, torch.device(device)
+        self.overlap = overlap
+        if overlap:
+            self.side = torch.cuda.Stream(device=self.dev)
+            self.ev_pyr = torch.cuda.Event()
+            self.ev_klt = torch.cuda.Event()
         self.B = cams * frames_per_step
         self.pitch = l0_pitch
         self.layout = v2d.pyramid_layout(cfg.W, cfg.H, cfg.levels)
@@ -75,21 +89,40 @@ class Frontend2D:
         (SURVEY §8(a) a7)."""
         c, B = self.cfg, self.B
         W, H, L = c.W, c.H, c.levels
+        st = self.status if status_out is None else status_out
+
+        def klt(lo, hi):  # images [lo, hi) of the step (frames lo/C .. hi/C - 1)
+            if hi <= lo:
+                return
+            v2d.track_klt_ptrs(prev_l0_ptrs[lo:hi], self.prev_pyr_ptrs[parity][lo:hi],
+                               l0_ptrs[lo:hi], self.pyr_ptrs[parity][lo:hi], self.pitch, hi - lo,
+                               W, H, L, self.kp_xy[:-1].reshape(B, self.P, 2)[lo:hi], None, None,
+                               self.P, c.win, c.iters, c.eps, c.ncc_min, c.min_eig,
+                               self.pos[lo:hi], st[lo:hi], self.ncc[lo:hi], self.iters[lo:hi],
+                               c.klt_flags, None if track_list is None else track_list[lo:hi])
+
         if events is not None:
             events[0].record()
         v2d.build_pyramid_ptrs(l0_ptrs, self.pitch, B, W, H, L, self.pyr_ptrs[parity])
         if events is not None:
             events[1].record()
+        if self.overlap:
+            main = torch.cuda.current_stream()
+            self.ev_pyr.record(main)
+            with torch.cuda.stream(self.side):
+                self.side.wait_event(self.ev_pyr)
+                klt(0, self.C)
+                self.ev_klt.record(self.side)
         v2d.detect_gftt_ptrs(l0_ptrs, self.pitch, B, W, H, c.grid_x, c.grid_y, c.k, c.K_min,
                              c.min_score, c.border, c.nms, self.kp_xy[1:], self.kp_score[1:],
                              self.cell_count[1:], workspace=self.ws)
         if events is not None:
             events[2].record()
-        st = self.status if status_out is None else status_out
-        v2d.track_klt_ptrs(prev_l0_ptrs, self.prev_pyr_ptrs[parity], l0_ptrs,
-                           self.pyr_ptrs[parity], self.pitch, B, W, H, L, self.kp_xy[:-1],
-                           None, None, self.P, c.win, c.iters, c.eps, c.ncc_min, c.min_eig,
-                           self.pos, st, self.ncc, self.iters, c.klt_flags, track_list)
+        if self.overlap:
+            klt(self.C, B)
+            torch.cuda.current_stream().wait_event(self.ev_klt)
+        else:
+            klt(0, B)
         if events is not None:
             events[3].record()
         self.kp_xy[0].copy_(self.kp_xy[-1], non_blocking=True)
