@@ -28,6 +28,18 @@
 // lane -> warp-uniform control flow).
 #include "common.cuh"
 
+#ifdef V2D_KLT_STATS  // debug builds only: event counters for the cost model
+__device__ unsigned long long g_klt_stats[16];
+#define KSTAT(i) \
+  do {           \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_klt_stats[i], 1ull); \
+  } while (0)
+#else
+#define KSTAT(i) \
+  do {           \
+  } while (0)
+#endif
+
 namespace v2d {
 namespace {
 
@@ -123,9 +135,11 @@ __device__ __forceinline__ void stage_f32(float* __restrict__ sp, int kPitch,
   const float* col = base + clampi(ox + lane, 0, W - 1);
   __syncwarp();
   if (oy >= 0 && oy + nr <= H) {
+    KSTAT(9);
     const float* p = col + (int64_t)oy * pitch;
     for (int r = 0; r < nr; ++r, p += pitch) cp_async4(sp + r * kPitch + lane, p);
   } else {  // clamp-to-edge rows: advance one pitch only while the next row is inside
+    KSTAT(10);
     const float* p = col + (int64_t)clampi(oy, 0, H - 1) * pitch;
     for (int r = 0; r < nr; ++r) {
       cp_async4(sp + r * kPitch + lane, p);
@@ -162,6 +176,7 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
   const int sh = ox & 3;
   if (ox >= 0 && ox + 32 <= W && oy >= 0 && oy + nr <= H && ox - sh + 36 <= pitch &&
       ((reinterpret_cast<uintptr_t>(base) | (uintptr_t)pitch) & 3) == 0) {
+    KSTAT(7);
     constexpr int kSP = 36;  // scratch bytes per row
     const int w = lane % 9, rr = lane / 9;
     const uint8_t* src = base + (int64_t)oy * pitch + (ox - sh) + 4 * w;
@@ -175,6 +190,7 @@ __device__ __noinline__ void stage_u8(float* __restrict__ sp, int kPitch,
     __syncwarp();
     return;
   }
+  KSTAT(8);
   const uint8_t* __restrict__ col = base + clampi(ox + lane, 0, W - 1);
   for (int r0 = 0; r0 < nr; r0 += 8) {
     unsigned v[8];
@@ -287,6 +303,7 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
     //   Ty(v) = [(1-ay)E(v) + ay E(v+1)]/8,     E(v) = Hs(v+2) - Hs(v)
     //   T(v)  = (1-ay)h(v+1) + ay h(v+2),       h = (1-ax)P1 + ax P2
     // swept down each run (v = run row).
+    KSTAT(1);
     const float2 wx = f2(ax, ax), wy = f2(ay, ay), two = f2(2.f, 2.f);
     float2 dx1 = f2(0.f, 0.f), dx2 = dx1;   // Dx rows q-2, q-1
     float2 hs1 = dx1, hs2 = dx1;            // Hs rows q-2, q-1
@@ -329,6 +346,7 @@ __device__ __forceinline__ void build_template(const float* __restrict__ P,
     // centre row lr advances by 0 or 1 per grid row (warp-uniform).  Every value
     // is exact in fp32 (a few multiples of 4^-L below 2^12), so the order of the
     // sums does not matter.
+    KSTAT(2);
     const int c = min(lane, WIN);
     const int lc = clampi(ix - R + c, 0, W - 1) - (ix - R - 1);
     const float* col = P + lc;
@@ -488,6 +506,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, ru, t);
   }
   out.levels++;
+  KSTAT(0);
   // per-run accumulation (.x run, .y run) -> no operand shuffling
   float2 axx = f2(0.f, 0.f), axy = axx, ayy = axx, ats = axx;
 #pragma unroll
@@ -511,6 +530,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   // b carries 8; every compensation below is a power of two, so all results are
   // bit-identical to the unscaled arithmetic.
   if (!finite || !(det > 0.0f) || det < a.min_eig * (float)N * lmax * 64.0f) {
+    KSTAT(6);
     if (L > 0) {
       dx *= 2.0f;
       dy *= 2.0f;
@@ -545,6 +565,8 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     lc0 = ixq - R - jx0;
     lr0 = iyq - R - jy0;
     if (!staged || lc0 < 0 || lc0 > 2 * M || lr0 < 0 || lr0 > 2 * M) {
+      KSTAT(4);
+      if (staged) KSTAT(5);
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
       stage(sp, Smem<WIN>::P, GX, J, jx0, jy0, SZ);
@@ -564,6 +586,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     dx += ex;
     dy += ey;
     out.steps++;
+    KSTAT(3);
     const float nx = cx + dx, ny = cy + dy;
     const bool inside = nx >= 0.0f && nx <= xmax && ny >= 0.0f && ny <= ymax;
     if (!inside) {  // (also false for NaN)
@@ -760,3 +783,16 @@ int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
 }
 
 }  // namespace v2d
+
+#ifdef V2D_KLT_STATS
+extern "C" int v2d_debug_klt_stats(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_klt_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return -1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_klt_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
