@@ -480,6 +480,20 @@ def main():
         tr = json.load(open(traffic_path))
         if roof["kernel"] in tr:
             roof["traffic"] = tr[roof["kernel"]]
+    # every kernel against its own roofline (the dominant one is `roofline`)
+    k1_ach = B * alg_bytes_pyramid(wl.W, wl.H, wl.levels) / (k_ms[0] * 1e-3) / 1e9
+    k2_ach = B * wl.W * wl.H * 40.0 / (k_ms[1] * 1e-3) / 1e12
+    k3_ach = klt_flops(iters_np, wl.win) / args.steps / (k_ms[2] * 1e-3) / 1e12
+    rooflines = {
+        "pyramid": {"bound": "hbm", "achieved": k1_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": k1_ach / pk["hbm_gbs"],
+                    "alg_bytes_per_image": alg_bytes_pyramid(wl.W, wl.H, wl.levels)},
+        "gftt_topk": {"bound": "alu", "achieved": k2_ach, "peak": pk["lane_ops_tops"],
+                      "unit": "Tlane-op/s", "frac": k2_ach / pk["lane_ops_tops"],
+                      "model": "40 lane-ops per L0 pixel (SURVEY §8(d))"},
+        "klt": {"bound": "alu", "achieved": k3_ach, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                "frac": k3_ach / pk["fp32_tflops"]},
+    }
     full_bytes = alg_bytes_full_path(wl.W, wl.H, wl.levels) * frames_total
     hbm_ach = full_bytes / (ms_max / 1e3) / 1e9 / world
     rig_per_step = B * world / C
@@ -500,6 +514,7 @@ def main():
                           "frac_of_8TBps_spec": hbm_ach / 8000.0,
                           "alg_bytes_per_camera_frame": alg_bytes_full_path(wl.W, wl.H, wl.levels)},
         "roofline": roof,
+        "rooflines_all_kernels": rooflines,
         "kernels": {n: {"ms_per_launch": float(k_ms[j]), "share_of_step": float(k_ms[j] / (ms / args.steps))}
                     for j, n in enumerate(names)},
         "gpu_launches": fe.launches_per_step * args.steps,

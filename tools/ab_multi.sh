@@ -1,7 +1,7 @@
 # Same-box comparison of several builds exp/lib_<V>.so x bench options.
 # usage: bash tools/ab_multi.sh "A P2 P3" "--overlap 0|--overlap 1" c5 c2
 VS=$1; OPTS=$2; shift 2
-IFS='|' read -ra OA <<< "$OPTS"
+IFS="|" read -ra OA <<< "$OPTS"; [ ${#OA[@]} -eq 0 ] && OA=("")
 for CFG in ${@:-c5}; do
   for i in 1 2; do
     for V in $VS; do
