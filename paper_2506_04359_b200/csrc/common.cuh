@@ -46,6 +46,14 @@ int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
                const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
                int32_t* iters_out, float* track_list, cudaStream_t st);
 
+// K3 for windows <= 13 (klt_pair.cu): two keypoints per warp
+bool klt_pair_supported(int win);
+int launch_klt_pair(const uint8_t* const* prev_l0, const float* const* prev_pyr,
+                    const uint8_t* const* next_l0, const float* const* next_pyr, int B,
+                    const Levels& lv, const KltArgs& a, const float* pts, const float* guess,
+                    const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
+                    int32_t* iters_out, float* track_list, cudaStream_t st);
+
 int launch_patches(const uint8_t* const* l0_ptrs, const float* const* pyr_ptrs, int64_t l0_pitch,
                    int B, const Levels& lv, const float* pts, int P, int patch, float* out,
                    cudaStream_t st);

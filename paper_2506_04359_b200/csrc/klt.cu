@@ -755,6 +755,11 @@ int launch_klt(const uint8_t* const* prev_l0, const float* const* prev_pyr,
                const uint8_t* in_status, float* out_pos, uint8_t* status, float* ncc,
                int32_t* iters_out, float* track_list, cudaStream_t st) {
   if (B == 0 || a.P == 0) return V2D_OK;
+#ifndef V2D_NO_PAIR
+  if (klt_pair_supported(a.win))  // small windows: two keypoints per warp (klt_pair.cu)
+    return launch_klt_pair(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a, pts, guess, in_status,
+                           out_pos, status, ncc, iters_out, track_list, st);
+#endif
 #define V2D_WIN_CASE(w)                                                                   \
   case w:                                                                                 \
     launch_win<w>(prev_l0, prev_pyr, next_l0, next_pyr, B, lv, a, pts, guess, in_status, \
