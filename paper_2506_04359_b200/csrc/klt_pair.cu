@@ -110,24 +110,31 @@ __device__ __forceinline__ void pstage(float* __restrict__ sp, int kPitch, const
                                        int ox, int oy, bool on) {
   const int lane16 = threadIdx.x & 15;
   __syncwarp();
+  // clamp-to-edge rows by pointer stepping: start at the clamped first row and
+  // advance one pitch only while the next row is inside (no per-row clamp/multiply)
+  const unsigned hm1 = (unsigned)(pl.H - 1);
   if (pl.u8) {
-    const uint8_t* col = reinterpret_cast<const uint8_t*>(pl.base) + pclampi(ox + lane16, 0, pl.W - 1);
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(pl.base) + pclampi(ox + lane16, 0, pl.W - 1) +
+                       (int64_t)pclampi(oy, 0, pl.H - 1) * pl.pitch;
     unsigned v[NR];
 #pragma unroll
-    for (int r = 0; r < NR; ++r)
-      v[r] = on ? __ldg(col + (int64_t)pclampi(oy + r, 0, pl.H - 1) * pl.pitch) : 0u;
+    for (int r = 0; r < NR; ++r) {
+      v[r] = on ? __ldg(p) : 0u;
+      if ((unsigned)(oy + r) < hm1) p += pl.pitch;
+    }
 #pragma unroll
     for (int r = 0; r < NR; ++r)
       if (on) sp[r * kPitch + lane16] = pu8_to_f32(v[r]);
   } else {
-    const float* col = reinterpret_cast<const float*>(pl.base) + pclampi(ox + lane16, 0, pl.W - 1);
+    const float* p = reinterpret_cast<const float*>(pl.base) + pclampi(ox + lane16, 0, pl.W - 1) +
+                     (int64_t)pclampi(oy, 0, pl.H - 1) * pl.pitch;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (on) {
         const unsigned d = (unsigned)__cvta_generic_to_shared(sp + r * kPitch + lane16);
-        const float* src = col + (int64_t)pclampi(oy + r, 0, pl.H - 1) * pl.pitch;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(p) : "memory");
       }
+      if ((unsigned)(oy + r) < hm1) p += pl.pitch;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
