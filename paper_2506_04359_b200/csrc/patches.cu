@@ -29,7 +29,9 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
                float* __restrict__ out) {
   constexpr int patch = PATCH;
   constexpr int n = patch * patch, r = (patch - 1) / 2, e = patch + 1, EE = e * e;
-  constexpr int kPerBatch = kBudget / EE > 0 ? kBudget / EE : 1;  // levels staged at once
+  // levels staged at once (<= the 8 a pyramid can have)
+  constexpr int kPerBatch = kBudget / EE < 1 ? 1 : (kBudget / EE > V2D_MAX_LEVELS ? V2D_MAX_LEVELS
+                                                                                   : kBudget / EE);
   constexpr int kLd = (EE + 31) / 32, kSm = (n + 31) / 32;         // per lane and level
   __shared__ float s_blk[kWarps][kPerBatch * EE];
   const int64_t kp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -66,7 +68,10 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
     __syncwarp();
     // ---- stage the (patch+1)^2 blocks of levels L0 .. L0+nb-1 (clamp-to-edge);
     // every load of the batch is independent, so all of them are in flight
-    for (int q = 0; q < nb; ++q) {
+    // (32-bit element offsets: a level plane or frame is < 2^31 elements)
+#pragma unroll
+    for (int q = 0; q < kPerBatch; ++q) {
+      if (q >= nb) break;
       const int L = L0 + q;
       const float scale = __int_as_float((127 - L) << 23);  // 2^-L
       const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
@@ -74,32 +79,36 @@ patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* _
       const int Wl = lv.W[L] - 1, Hl = lv.H[L] - 1;
       float* dst = blk + q * EE;
       if (L == 0) {
+        const int pitch = (int)l0_pitch;
 #pragma unroll
         for (int m = 0; m < kLd; ++m) {
           const int x = min(max(bx + bc[m], 0), Wl), y = min(max(by + br[m], 0), Hl);
-          const float v = (float)__ldg(l0 + (int64_t)y * l0_pitch + x);
+          const float v = (float)__ldg(l0 + (unsigned)(y * pitch + x));
           if (lane + 32 * m < EE) dst[lane + 32 * m] = v;
         }
       } else {
         const float* pl = pyr + lv.offset[L];
-        const int64_t pitch = lv.pitch[L];
+        const int pitch = (int)lv.pitch[L];
 #pragma unroll
         for (int m = 0; m < kLd; ++m) {
           const int x = min(max(bx + bc[m], 0), Wl), y = min(max(by + br[m], 0), Hl);
-          const float v = __ldg(pl + (int64_t)y * pitch + x);
+          const float v = __ldg(pl + (unsigned)(y * pitch + x));
           if (lane + 32 * m < EE) dst[lane + 32 * m] = v;
         }
       }
     }
     __syncwarp();
     // ---- samples of those levels, stored contiguously ([L][v][u])
-    for (int q = 0; q < nb; ++q) {
+    float* oL0 = o + L0 * n + lane;
+#pragma unroll
+    for (int q = 0; q < kPerBatch; ++q) {
+      if (q >= nb) break;
       const int L = L0 + q;
       const float scale = __int_as_float((127 - L) << 23);
       const float cx = (px0 + 0.5f) * scale - 0.5f, cy = (py0 + 0.5f) * scale - 0.5f;
       const float wa = cx - floorf(cx), wb = cy - floorf(cy);
       const float* src = blk + q * EE;
-      float* oL = o + L * n;
+      float* oL = oL0 + q * n - lane;
 #pragma unroll
       for (int m = 0; m < kSm; ++m) {
         const float* t = src + sv[m] * e + su[m];
