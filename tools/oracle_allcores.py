@@ -21,7 +21,7 @@ def worker(args):
     st = bench.OracleStream(synth.WORKLOADS[cfg], salt=salt)
     n, tracked, t0 = 0, 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds:
-        tr, _ = st.step()
+        tr, _, _, _ = st.step()
         tracked += tr
         n += 1
     return n, tracked, time.perf_counter() - t0
