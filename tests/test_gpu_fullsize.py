@@ -147,3 +147,41 @@ def test_multistep_stream_parity_c2():
         assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
         assert stats["flips_unattributable"] == 0, stats
         assert stats["both_tracked"] > 0.5 * len(pick), (s, stats)
+
+
+@pytest.mark.parametrize("name,win,each", [("c5", 11, False), ("c5", 13, False),
+                                           ("c4", 11, True), ("c5", 21, True)])
+def test_fullsize_klt_variants_sampled(name, win, each):
+    """The f3 variants at full size on the bench data: the two-keypoints-per-warp
+    kernel (windows <= 13) and NCC at every Gauss-Newton step, sampled keypoints
+    of sampled images recomputed by the oracle, strict KLT bar."""
+    wl, st, fe, sched, F = _setup(name)
+    C = wl.cams
+    B = F * C
+    frames = st.frames.cpu().numpy()
+    cur, prev, parity = sched.tables(0)
+    pts = fe.tracked_pts.reshape(B, fe.P, 2).contiguous()
+    pos, stt, nc, it = (torch.empty_like(fe.pos), torch.empty_like(fe.status),
+                        torch.empty_like(fe.ncc), torch.empty_like(fe.iters))
+    v2d.track_klt_ptrs(prev, fe.prev_pyr_ptrs[parity], cur, fe.pyr_ptrs[parity], fe.pitch, B,
+                       wl.W, wl.H, wl.levels, pts, None, None, fe.P, win, wl.iters, wl.eps,
+                       wl.ncc_min, wl.min_eig, pos, stt, nc, it,
+                       v2d.KLT_NCC_EACH_STEP if each else 0)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(win * 31 + each)
+    for b in sorted(set(rng.choice(B, size=2, replace=False).tolist())):
+        f, c = divmod(b, C)
+        _, d_prv = oracle.build_pyramid(frames[c, (f - 1) % frames.shape[1], :, :wl.W], wl.levels)
+        _, d_cur = oracle.build_pyramid(frames[c, f % frames.shape[1], :, :wl.W], wl.levels)
+        pa = pts[b].cpu().numpy()
+        valid = np.nonzero(pa[:, 0] >= 0)[0]
+        pick = rng.choice(valid, size=min(80, len(valid)), replace=False)
+        opos, ost, onc, dg = oracle.track_klt(d_prv, d_cur, wl.W, wl.H, wl.levels, pa[pick],
+                                              win=win, iters=wl.iters, eps=wl.eps,
+                                              ncc_min=wl.ncc_min, min_eig=wl.min_eig,
+                                              ncc_each_step=each)
+        stats = compare_klt(pa[pick], pos[b].cpu().numpy()[pick], stt[b].cpu().numpy()[pick],
+                            opos, ost, dg)
+        assert stats["pos_over_tol"] == 0 and stats["max_pos_err"] <= POS_TOL, stats
+        assert stats["flips_unattributable"] == 0, stats
+        assert stats["both_tracked"] > 0.5 * len(pick), stats
