@@ -103,12 +103,13 @@ def test_fullsize_tracking_quality_c2():
     assert np.median(e) < 0.05 and np.mean(e < 0.2) > 0.95
 
 
-def test_multistep_stream_parity_c2():
+@pytest.mark.parametrize("name,F,steps", [("c2", 4, 4), ("c5", 1, 3)])
+def test_multistep_stream_parity(name, F, steps):
     """Several consecutive steps of the bench configuration (pyramid parity double
     buffer, keypoint carry from the last frame of a step to the first of the
     next): sampled selections and tracks of every step agree with the oracle."""
-    wl = synth.WORKLOADS["c2"]
-    C, F, steps = wl.cams, 4, 4
+    wl = synth.WORKLOADS[name]
+    C = wl.cams
     cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
                              grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
                              win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
