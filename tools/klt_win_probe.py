@@ -15,6 +15,7 @@ from paper_2506_04359_b200.frontend import RingSchedule  # noqa: E402
 
 win = int(sys.argv[1]) if len(sys.argv) > 1 else 11
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+levels_arg = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # track through fewer levels
 wl = synth.WORKLOADS["c5"]
 lay = bench.bench_layout(wl, 1)
 st = synth.make_stream(wl, lay["R"], "cuda")
@@ -29,7 +30,7 @@ pos = torch.empty_like(fe.pos)
 stt = torch.empty_like(fe.status)
 it = torch.empty_like(fe.iters)
 args = (prev, fe.prev_pyr_ptrs[parity], cur, fe.pyr_ptrs[parity], fe.pitch, fe.B, c.W, c.H,
-        c.levels, pts, None, None, fe.P, win, c.iters, c.eps, c.ncc_min, c.min_eig, pos, stt,
+        levels_arg or c.levels, pts, None, None, fe.P, win, c.iters, c.eps, c.ncc_min, c.min_eig, pos, stt,
         None, it)
 v2d.track_klt_ptrs(*args)
 torch.cuda.synchronize()
@@ -39,5 +40,5 @@ for _ in range(reps):
     v2d.track_klt_ptrs(*args)
 b.record()
 torch.cuda.synchronize()
-print(f"win {win}: {a.elapsed_time(b) / reps:.4f} ms per launch, "
+print(f"win {win} levels {levels_arg or c.levels}: {a.elapsed_time(b) / reps:.4f} ms per launch, "
       f"steps/kp {float((it & 0xFFFFFF).sum()) / max(1, int((stt != 4).sum())):.2f}")
