@@ -40,6 +40,39 @@ __device__ unsigned long long g_klt_stats[16];
   } while (0)
 #endif
 
+#ifdef V2D_KLT_CYC  // debug builds only: phase cycles (warp-elapsed SM clocks) kept in
+// per-warp registers and flushed once per warp into one of 64 slots (no atomics inside
+// the timed phases):
+// 0 template staging, 1 template build + G + eigen test + Stt, 2 search staging,
+// 3 Gauss-Newton steps (staging excluded), 4 NCC gate, 5 whole warp
+__device__ unsigned long long g_klt_cyc[64][8];
+#define KCLK(v) const unsigned v = (unsigned)clock()
+#define KCYC(ph, t0) kc[ph] += (unsigned)clock() - (t0)
+#define KCYC_DECL unsigned kc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define KCYC_PARAM , unsigned* kc
+#define KCYC_ARG , kc
+#define KCYC_FLUSH                                                              \
+  do {                                                                          \
+    if ((threadIdx.x & 31) == 0)                                                \
+      for (int i = 0; i < 6; ++i) atomicAdd(&g_klt_cyc[blockIdx.x & 63][i], (unsigned long long)kc[i]); \
+  } while (0)
+#else
+#define KCLK(v) \
+  do {          \
+  } while (0)
+#define KCYC(ph, t0) \
+  do {               \
+  } while (0)
+#define KCYC_DECL \
+  do {            \
+  } while (0)
+#define KCYC_PARAM
+#define KCYC_ARG
+#define KCYC_FLUSH \
+  do {             \
+  } while (0)
+#endif
+
 namespace v2d {
 namespace {
 
@@ -485,7 +518,7 @@ template <int WIN, bool kEachStep>
 __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const Plane& I,
                                                  const Plane& J, const int L, const float cx,
                                                  const float cy, float& dx, float& dy,
-                                                 const KltArgs& a, LevelOut& out) {
+                                                 const KltArgs& a, LevelOut& out KCYC_PARAM) {
   constexpr int R = (WIN - 1) / 2;
   constexpr int N = WIN * WIN;
   constexpr int M = search_margin(WIN);  // staged motion margin (px)
@@ -502,7 +535,14 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   {
     const float fcx = floorf(cx), fcy = floorf(cy);
     const int ix = (int)fcx, iy = (int)fcy;
+    KCLK(t_st);
     stage(sp, Smem<WIN>::P, GX, I, ix - R - 1, iy - R - 1, WIN + 3);
+    KCYC(0, t_st);
+  }
+  KCLK(t_tm);
+  {
+    const float fcx = floorf(cx), fcy = floorf(cy);
+    const int ix = (int)fcx, iy = (int)fcy;
     build_template<WIN>(sp, GX, GY, ix, iy, cx - fcx, cy - fcy, I.W, I.H, ru, t);
   }
   out.levels++;
@@ -531,6 +571,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   // bit-identical to the unscaled arithmetic.
   if (!finite || !(det > 0.0f) || det < a.min_eig * (float)N * lmax * 64.0f) {
     KSTAT(6);
+    KCYC(1, t_tm);
     if (L > 0) {
       dx *= 2.0f;
       dy *= 2.0f;
@@ -552,6 +593,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     q = fma2(d, d, q);
   }
   const float Stt = warp_sum2(f2(ru.sum2(q), 0.f)).x;
+  KCYC(1, t_tm);
 
   // ---------------- Gauss-Newton iterations (next frame) --------------------
   const float xmax = (float)(J.W - 1), ymax = (float)(J.H - 1);
@@ -569,13 +611,16 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
       if (staged) KSTAT(5);
       jx0 = ixq - R - M;
       jy0 = iyq - R - M;
+      KCLK(t_ss);
       stage(sp, Smem<WIN>::P, GX, J, jx0, jy0, SZ);
+      KCYC(2, t_ss);
       staged = true;
       lc0 = M;
       lr0 = M;
     }
   };
   const float eps2 = a.eps * a.eps;
+  KCLK(t_gn);
   for (int it = 1; it <= a.iters; ++it) {
     int lc0, lr0;
     float bx, by;
@@ -616,6 +661,8 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     if (fmaf(ex, ex, ey * ey) < eps2) break;
   }
   // ---------------- per-level NCC gate --------------------------------------
+  KCYC(3, t_gn);
+  KCLK(t_nc);
   {
     int lc0, lr0;
     float bx, by;
@@ -629,6 +676,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     const float Sts = r2;
     const float den2 = Stt * Sss;
     out.ncc = den2 > 0.0f ? Sts * rsqrtf(den2) : 0.0f;
+    KCYC(4, t_nc);
     if (out.ncc < a.ncc_min) {
       out.status = V2D_LOST_NCC;
       return;
@@ -647,10 +695,10 @@ template <int WIN, bool kEachStep>
 __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane I, const Plane J,
                                             const int L, const float cx, const float cy,
                                             float& dx_io, float& dy_io, const KltArgs a,
-                                            LevelOut& out_io) {
+                                            LevelOut& out_io KCYC_PARAM) {
   float dx = dx_io, dy = dy_io;
   LevelOut out = out_io;
-  track_level_body<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, out);
+  track_level_body<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, out KCYC_ARG);
   dx_io = dx;
   dy_io = dy;
   out_io = out;
@@ -672,6 +720,8 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
   const int b = (int)(warp / a.P);
   const float px = pts[2 * warp], py = pts[2 * warp + 1];
   constexpr int R = (WIN - 1) / 2;
+  KCLK(t_all);
+  KCYC_DECL;
 
   LevelOut o{V2D_TRACKED, 0.0f, 0, 0};
   const bool skip = (in_status && in_status[warp] != 0) || (px == -1.0f && py == -1.0f) ||
@@ -699,7 +749,7 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
         I = Plane{prev_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
         J = Plane{next_pyr[b] + lv.offset[L], lv.pitch[L], lv.W[L], lv.H[L], 0};
       }
-      track_level<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, o);
+      track_level<WIN, kEachStep>(sp, I, J, L, cx, cy, dx, dy, a, o KCYC_ARG);
     }
   }
   float ox = -1.0f, oy = -1.0f;
@@ -722,6 +772,8 @@ klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __res
     // a7 track-list record (x, y, status, ncc): the rig-wide all-gather ships these
     if (track_list) track_list[warp] = make_float4(ox, oy, (float)o.status, o.ncc);
   }
+  KCYC(5, t_all);
+  KCYC_FLUSH;
 }
 
 template <int WIN>
@@ -797,6 +849,18 @@ extern "C" int v2d_debug_klt_stats(unsigned long long* out, int reset) {
   if (reset) {
     unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_klt_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+#ifdef V2D_KLT_CYC
+extern "C" int v2d_debug_klt_cycles(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_klt_cyc, sizeof(unsigned long long) * 512) != cudaSuccess)
+    return -1;
+  if (reset) {
+    unsigned long long z[512] = {0};
+    cudaMemcpyToSymbol(g_klt_cyc, z, sizeof(z));
   }
   return 0;
 }
