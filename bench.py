@@ -137,20 +137,74 @@ def klt_flops(iters_packed: np.ndarray, win: int) -> float:
 # clocks sampler
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region:
+    NVML polled from a thread every ~5 ms (so even a 20-step run gets samples); the
+    nvidia-smi -lms 50 stream is the fallback when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.proc = None
         self.idx = gpu_index
-        if shutil.which("nvidia-smi"):
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.nvml = None
+        self.samples = []
+        try:
+            self._start_nvml(gpu_index)
+        except Exception:
+            self.nvml = None
+            if shutil.which("nvidia-smi"):
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+    def _start_nvml(self, gpu_index):
+        import threading
+
+        import pynvml as nv
+        import torch
+        nv.nvmlInit()
+        try:  # the CUDA device's own GPU (CUDA_VISIBLE_DEVICES may renumber)
+            h = nv.nvmlDeviceGetHandleByUUID(
+                "GPU-" + str(torch.cuda.get_device_properties(gpu_index).uuid))
+        except Exception:
+            h = nv.nvmlDeviceGetHandleByIndex(gpu_index)
+        self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        self.nvml = nv
+        self.stop_flag = threading.Event()
+
+        def poll():
+            while not self.stop_flag.is_set():
+                try:
+                    mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((mhz, {n for n, bt in bits.items() if r & bt}))
+                except Exception:
+                    pass
+                time.sleep(0.005)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        t0 = time.perf_counter()
+        while not self.samples and time.perf_counter() - t0 < 1.0:
+            time.sleep(0.001)  # the first sample precedes the timed region
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            if not self.samples:
+                return None
+            reasons = set().union(*(r for _, r in self.samples))
+            return {"sm_mhz": float(np.median([m for m, _ in self.samples])),
+                    "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                    "reasons": sorted(reasons), "source": "nvml, polled every 5 ms"}
         if self.proc is None:
             return None
         time.sleep(0.25)
@@ -161,7 +215,6 @@ class Clocks:
             self.proc.kill()
             out, _ = self.proc.communicate()
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
@@ -171,13 +224,13 @@ class Clocks:
                 mx = max(mx, float(f[2]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(self.NAMES, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "source": "nvidia-smi -lms 50"}
 
 
 # ---------------------------------------------------------------------------
