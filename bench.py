@@ -779,13 +779,14 @@ def run_variants(fe, sched, args, wl, F, C, reps=20):
 
 
 def run_f1(fe, sched, C, n_eager=60, n_graph=200):
-    """Variant f1 timed three ways on the bench ring: the natural loop (T = 0.7,
-    keyframes when fewer than 70 % of the keyframe's tracks survive, Eq. 5),
-    eager and replayed as CUDA graphs, with its keyframe rate counted on the
-    device; and two graph-replayed bounds that isolate the keyframe branch
-    (suppression mask + masked detection + refill): T = 1.01 takes it every
-    frame, T = 0 never (after the bootstrap keyframe).  branch_ms = their
-    difference per rig-frame."""
+    """Variant f1 timed on the bench ring: the natural loop (T = 0.7, keyframes when
+    fewer than 70 % of the keyframe's tracks survive, Eq. 5), eager and replayed as
+    CUDA graphs — one graph launch per rig-frame, the keyframe branch the body of a
+    conditional IF node set by the decide kernel; also the flag-gated torch-graph
+    form for comparison — with its keyframe rate counted on the device; and two
+    graph-replayed bounds that isolate the keyframe branch (suppression mask +
+    masked detection + refill): T = 1.01 takes it every frame, T = 0 never (after
+    the bootstrap keyframe).  branch_ms = their difference per rig-frame."""
     import torch
 
     from paper_2506_04359_b200.frontend import KeyframeTracker
@@ -809,8 +810,8 @@ def run_f1(fe, sched, C, n_eager=60, n_graph=200):
     res["ms_per_rig_frame_eager"] = a.elapsed_time(b) / (n_eager - 2)
     res["keyframe_rate_eager"] = float(kfs.item()) / (n_eager - 2)
 
-    def graph_ms(tracker, t0):
-        tracker.capture(table, t0)
+    def graph_ms(tracker, t0, conditional=True):
+        tracker.capture(table, t0, conditional=conditional)
         for _ in range(2):
             tracker.replay()
         torch.cuda.synchronize()
@@ -824,18 +825,33 @@ def run_f1(fe, sched, C, n_eager=60, n_graph=200):
 
     ms_g, rate = graph_ms(kt, n_eager)
     res.update({"ms_per_rig_frame_graph": ms_g, "camera_frames_per_s_graph": C / (ms_g * 1e-3),
-                "keyframe_rate_graph": rate,
+                "keyframe_rate_graph": rate, "graph_kind": kt.graph_kind,
                 "alive_fraction_end": float((kt.table()[1] == 0).float().mean())})
     del kt
+    # the same loop captured with torch.cuda.graph: the keyframe branch's five kernels
+    # are launched every frame and exit on the device flag (round-1/2 form)
+    kt = KeyframeTracker(c, C, dev, fe.pitch, T=0.7)
+    kt.start(frame_ptr(0))
+    for t in range(1, n_eager):
+        kt.step(frame_ptr(t), frame_ptr(t - 1))
+    ms_t, rate_t = graph_ms(kt, n_eager, conditional=False)
+    res["flag_gated_graph"] = {"ms_per_rig_frame_graph": ms_t, "keyframe_rate": rate_t,
+                               "graph_kind": kt.graph_kind}
+    del kt
     for name, T in (("always_keyframe", 1.01), ("never_keyframe", 0.0)):
-        kb = KeyframeTracker(c, C, dev, fe.pitch, T=T)
-        kb.start(frame_ptr(0))
-        ms_b, rate_b = graph_ms(kb, 1)
-        res[name] = {"T": T, "ms_per_rig_frame_graph": ms_b, "keyframe_rate": rate_b}
-        del kb
+        for cond in (True, False):
+            kb = KeyframeTracker(c, C, dev, fe.pitch, T=T)
+            kb.start(frame_ptr(0))
+            ms_b, rate_b = graph_ms(kb, 1, conditional=cond)
+            key = name if cond else name + "_flag_gated"
+            res[key] = {"T": T, "ms_per_rig_frame_graph": ms_b, "keyframe_rate": rate_b,
+                        "graph_kind": kb.graph_kind}
+            del kb
     res["keyframe_branch_ms_per_rig_frame"] = (res["always_keyframe"]["ms_per_rig_frame_graph"] -
                                                res["never_keyframe"]["ms_per_rig_frame_graph"])
-    res.update({"min_separation_px": float(c.win // 2), "launches_per_frame": 8,
+    res.update({"min_separation_px": float(c.win // 2),
+                "launches_per_frame": {"eager": 9, "graph_conditional": "5 (+5 in the IF body "
+                                       "on keyframes)", "graph_flag_gated": 10},
                 "camera_frames_per_s_eager": C / (res["ms_per_rig_frame_eager"] * 1e-3)})
     torch.cuda.empty_cache()
     return res

@@ -188,6 +188,25 @@ int v2d_track_survival(const uint8_t* status, const uint8_t* kf_member, int B, i
 int v2d_keyframe_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
                         v2d_stream_t stream);
 
+/* v2d_keyframe_decide for the f1 loop recorded as one CUDA graph per frame: the same
+ * decision into *flag, then kf_count[0] += *flag (nullable int64[1]: keyframes so far)
+ * and, if cond_handle != 0, cudaGraphSetConditional(cond_handle, *flag).  cond_handle
+ * is the value of a cudaGraphConditionalHandle (CUDA >= 12.3) of the graph this launch
+ * is captured into, whose IF node holds the keyframe branch (suppress, detect, refill):
+ * on non-keyframe frames those kernels are then skipped by the device instead of
+ * launched to exit on *flag.  cond_handle must be 0 outside such a graph (then this is
+ * v2d_keyframe_decide plus the counter). */
+int v2d_keyframe_decide_graph(const int32_t* counts, int n, float T, int32_t* flag,
+                              int64_t* totals, int64_t* kf_count, uint64_t cond_handle,
+                              v2d_stream_t stream);
+
+/* Frame tables of a captured streaming loop (the graph replays with no host work):
+ * t = *counter; cur[c] = table[t mod R][c], prev[c] = table[(t-1) mod R][c] for
+ * c < C (device pointers as int64; table: device int64 [R][C]); then *counter = t+1.
+ * V2D_EINVAL: R < 1, C < 1 or > 65535, null pointer. */
+int v2d_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
+                    int64_t* prev, v2d_stream_t stream);
+
 /* If *flag: the j-th valid detection of image b (cell-major slot order of
  * v2d_detect_gftt's kp_xy, the first cell_count slots of each cell) fills the
  * j-th dead slot (ascending): status := V2D_TRACKED, id := next_id + j; then

@@ -41,7 +41,7 @@ int grid_k(int gx, int gy, int k, int K_min, int* k_out) {
 
 extern "C" {
 
-int v2d_version(void) { return 200; }
+int v2d_version(void) { return 201; }
 
 const char* v2d_strerror(int code) {
   switch (code) {
@@ -170,7 +170,24 @@ int v2d_track_survival(const uint8_t* status, const uint8_t* kf_member, int B, i
 int v2d_keyframe_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
                         v2d_stream_t stream) {
   if (n < 0 || !flag || (n > 0 && !counts) || !(T >= 0.0f)) return V2D_EINVAL;
-  return v2d::launch_decide(counts, n, T, flag, totals, reinterpret_cast<cudaStream_t>(stream));
+  return v2d::launch_decide(counts, n, T, flag, totals, nullptr, 0ull,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_keyframe_decide_graph(const int32_t* counts, int n, float T, int32_t* flag,
+                              int64_t* totals, int64_t* kf_count, uint64_t cond_handle,
+                              v2d_stream_t stream) {
+  if (n < 0 || !flag || (n > 0 && !counts) || !(T >= 0.0f)) return V2D_EINVAL;
+  return v2d::launch_decide(counts, n, T, flag, totals, kf_count,
+                            (unsigned long long)cond_handle,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int v2d_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
+                    int64_t* prev, v2d_stream_t stream) {
+  if (R < 1 || C < 1 || C > 65535 || !table || !counter || !cur || !prev) return V2D_EINVAL;
+  return v2d::launch_ring_tables(table, R, C, counter, cur, prev,
+                                 reinterpret_cast<cudaStream_t>(stream));
 }
 
 int v2d_refill_tracks(const float* kp_xy, const int32_t* cell_count, int grid_x, int grid_y,

@@ -67,7 +67,9 @@ int launch_suppress(uint8_t* const* mask_ptrs, int64_t pitch, int B, int W, int 
 int launch_survival(const uint8_t* status, const uint8_t* kf_member, int B, int P, int32_t* counts,
                     cudaStream_t st);
 int launch_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
-                  cudaStream_t st);
+                  int64_t* kf_count, unsigned long long cond, cudaStream_t st);
+int launch_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
+                       int64_t* prev, cudaStream_t st);
 int launch_refill(const float* kp_xy, const int32_t* cell_count, int cells, int k,
                   const int32_t* flag, int B, int P, float* tracks, uint8_t* status,
                   uint8_t* kf_member, int32_t* track_id, int32_t* next_id, cudaStream_t st);

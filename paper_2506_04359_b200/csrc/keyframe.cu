@@ -16,7 +16,10 @@
 //              next_id + j; then S_kf := the alive slots.  Lost slots never come
 //              back to life except by refill with a NEW id.
 // All are tiny, launch-latency-bound kernels; every one of them reads a device
-// flag so that the keyframe branch runs without a host round trip.
+// flag so that the keyframe branch runs without a host round trip.  Captured as one
+// CUDA graph per frame (frontend.KeyframeTracker.capture), the branch is the body of
+// a conditional (IF) node set by the decide kernel, and the frame tables come from a
+// device frame counter (ring_tables): one graph launch per rig-frame.
 #include "common.cuh"
 
 namespace v2d {
@@ -96,18 +99,39 @@ __global__ void survival_kernel(const uint8_t* __restrict__ status,
 }
 
 __global__ void decide_kernel(const int32_t* __restrict__ counts, int n, float T,
-                              int32_t* __restrict__ flag, int64_t* __restrict__ totals) {
+                              int32_t* __restrict__ flag, int64_t* __restrict__ totals,
+                              int64_t* __restrict__ kf_count, unsigned long long cond) {
   if (threadIdx.x != 0) return;
   int64_t nk = 0, ns = 0;
   for (int i = 0; i < n; ++i) {
     nk += counts[2 * i];
     ns += counts[2 * i + 1];
   }
-  flag[0] = (nk == 0 || (double)ns < (double)T * (double)nk) ? 1 : 0;
+  const int f = (nk == 0 || (double)ns < (double)T * (double)nk) ? 1 : 0;
+  flag[0] = f;
   if (totals) {
     totals[0] = nk;
     totals[1] = ns;
   }
+  if (kf_count) kf_count[0] += f;
+  // captured f1 loop: the keyframe branch is the body of a conditional (IF) graph node
+  // whose handle this sets, so on non-keyframe frames its kernels are not launched at all
+  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, (unsigned)f);
+}
+
+// Frame tables of a captured streaming loop: t = *counter, cur/prev = rows t and t-1
+// (mod R) of the [R][C] device-pointer table, then *counter = t + 1.
+__global__ void ring_tables_kernel(const int64_t* __restrict__ table, int R, int C,
+                                   int64_t* __restrict__ counter, int64_t* __restrict__ cur,
+                                   int64_t* __restrict__ prev) {
+  const int64_t t = counter[0];
+  const int64_t rc = ((t % R) + R) % R, rp = (((t - 1) % R) + R) % R;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    cur[c] = table[rc * C + c];
+    prev[c] = table[rp * C + c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) counter[0] = t + 1;
 }
 
 // Block exclusive scan of one int per thread; returns the block total.
@@ -212,8 +236,14 @@ int launch_survival(const uint8_t* status, const uint8_t* kf_member, int B, int 
 }
 
 int launch_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
-                  cudaStream_t st) {
-  decide_kernel<<<1, 32, 0, st>>>(counts, n, T, flag, totals);
+                  int64_t* kf_count, unsigned long long cond, cudaStream_t st) {
+  decide_kernel<<<1, 32, 0, st>>>(counts, n, T, flag, totals, kf_count, cond);
+  return cudaGetLastError() == cudaSuccess ? V2D_OK : V2D_ECUDA;
+}
+
+int launch_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
+                       int64_t* prev, cudaStream_t st) {
+  ring_tables_kernel<<<1, 128, 0, st>>>(table, R, C, counter, cur, prev);
   return cudaGetLastError() == cudaSuccess ? V2D_OK : V2D_ECUDA;
 }
 

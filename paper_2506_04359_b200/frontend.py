@@ -363,41 +363,113 @@ class KeyframeTracker:
         self.cur = j
 
     # ------------------------------------------------------------ CUDA graphs
-    def capture(self, frame_table: torch.Tensor, next_frame: int):
+    def _main(self, l0_ptrs, prev_l0_ptrs, j, cond_handle=0):
+        """The unconditional part of a frame (pyramid, KLT, survival, decide)."""
+        c, C, P = self.cfg, self.C, self.P
+        i = 1 - j
+        v2d.build_pyramid_ptrs(l0_ptrs, self.pitch, C, c.W, c.H, c.levels, self.pyr_ptrs[j])
+        v2d.track_klt_ptrs(prev_l0_ptrs, self.pyr_ptrs[i], l0_ptrs, self.pyr_ptrs[j], self.pitch,
+                           C, c.W, c.H, c.levels, self.tracks[i], None, self.status[i], P, c.win,
+                           c.iters, c.eps, c.ncc_min, c.min_eig, self.tracks[j], self.status[j],
+                           self.ncc, self.iters, c.klt_flags)
+        v2d.track_survival(self.status[j], self.kf_member, self.counts)
+        v2d.keyframe_decide_graph(self.counts, self.T, self.flag, self.totals, self.kf_count,
+                                  cond_handle)
+
+    def capture(self, frame_table: torch.Tensor, next_frame: int, conditional: bool = True):
         """Record the per-frame step as CUDA graphs (the loop is launch-bound: 8+
         small launches per rig-frame).  frame_table: device int64 [R, C] frame
         pointers, frame t = row t % R; next_frame: index of the next frame to
-        process.  The frame tables are gathered on the device from a device frame
-        counter, so replay() needs no host work besides one graph launch; one
-        graph per track-table parity.  Single-process only (group is None)."""
+        process.  The frame tables come from a device frame counter (v2d_ring_tables),
+        so replay() needs no host work besides one graph launch; one graph per
+        track-table parity.  conditional=True (default) builds each graph with the
+        CUDA graph API (cuda-python): the keyframe branch is the body of an IF node
+        whose value the decide kernel sets (v2d_keyframe_decide_graph), so a
+        non-keyframe frame runs 5 kernels and no empty grids; conditional=False (or
+        no conditional-node support) captures with torch.cuda.graph, the branch's
+        kernels exiting on the device flag.  Single-process only (group is None)."""
         assert self.group is None, "graph capture of the multi-GPU all-reduce is not supported"
-        R = frame_table.shape[0]
-        self._ft = frame_table
+        self._ft = frame_table.contiguous()
         self._t = torch.full((1,), next_frame, dtype=torch.int64, device=self.dev)
         self._l0 = torch.empty((self.C,), dtype=torch.int64, device=self.dev)
         self._pl0 = torch.empty((self.C,), dtype=torch.int64, device=self.dev)
-
-        def body():
-            self._l0.copy_(self._ft.index_select(0, torch.remainder(self._t, R)).view(-1))
-            self._pl0.copy_(self._ft.index_select(0, torch.remainder(self._t - 1, R)).view(-1))
-            self.step(self._l0, self._pl0)
-            self.kf_count.add_(self.flag[0])
-            self._t.add_(1)
-
         torch.cuda.synchronize(self.dev)
-        self._graphs = {}
+        self._graphs, self._execs = {}, {}
         cur0 = self.cur
-        for par in (cur0, 1 - cur0):  # step() toggles self.cur during capture
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                body()
-            self._graphs[par] = g
-        assert self.cur == cur0
+        self.graph_kind = "torch"
+        if conditional:
+            try:
+                for par in (cur0, 1 - cur0):
+                    self._execs[par] = self._capture_conditional(1 - par)
+                self.graph_kind = "conditional"
+            except Exception as e:  # no conditional nodes (driver / cuda-python): fallback
+                self._execs = {}
+                self.graph_fallback_reason = f"{type(e).__name__}: {e}"
+        if not self._execs:
+            for par in (cur0, 1 - cur0):
+                j = 1 - par
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    v2d.ring_tables(self._ft, self._t, self._l0, self._pl0)
+                    self._main(self._l0, self._pl0, j)
+                    self._keyframe_branch(self._l0, j)
+                self._graphs[par] = g
+        self.cur = cur0
         torch.cuda.synchronize(self.dev)
+
+    def _capture_conditional(self, j):
+        """One frame (parity: KLT writes table j) as a CUDA graph whose keyframe branch
+        is the body of a conditional IF node: ring tables -> pyramid -> KLT ->
+        survival -> decide (sets the node's value) -> IF(flag){suppress, detect,
+        refill}."""
+        from cuda.bindings import runtime as rt
+
+        def ok(r):  # cuda-python returns (err, *outputs)
+            r = r if isinstance(r, tuple) else (r,)
+            if r[0] != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"CUDA graph API: {r[0]}")
+            return None if len(r) == 1 else (r[1] if len(r) == 2 else r[1:])
+
+        graph = ok(rt.cudaGraphCreate(0))
+        handle = ok(rt.cudaGraphConditionalHandleCreate(graph, 0, 0))
+        s = torch.cuda.Stream(self.dev)
+        mode = rt.cudaStreamCaptureMode.cudaStreamCaptureModeThreadLocal
+        with torch.cuda.stream(s):
+            ok(rt.cudaStreamBeginCaptureToGraph(s.cuda_stream, graph, None, None, 0, mode))
+            v2d.ring_tables(self._ft, self._t, self._l0, self._pl0)
+            self._main(self._l0, self._pl0, j, int(handle))
+            ok(rt.cudaStreamEndCapture(s.cuda_stream))
+        # the captured main part is a chain: its one leaf node precedes the IF node
+        nodes, n = ok(rt.cudaGraphGetNodes(graph, 0))
+        nodes, n = ok(rt.cudaGraphGetNodes(graph, n))
+        leaves = [nd for nd in nodes if ok(rt.cudaGraphNodeGetDependentNodes(nd, 0))[1] == 0]
+        assert len(leaves) == 1, len(leaves)
+        params = rt.cudaGraphNodeParams()
+        params.type = rt.cudaGraphNodeType.cudaGraphNodeTypeConditional
+        params.conditional.handle = handle
+        params.conditional.type = rt.cudaGraphConditionalNodeType.cudaGraphCondTypeIf
+        params.conditional.size = 1
+        ok(rt.cudaGraphAddNode(graph, leaves, 1, params))
+        body = params.conditional.phGraph_out[0]
+        with torch.cuda.stream(s):
+            ok(rt.cudaStreamBeginCaptureToGraph(s.cuda_stream, body, None, None, 0, mode))
+            self._keyframe_branch(self._l0, j)
+            ok(rt.cudaStreamEndCapture(s.cuda_stream))
+        exe = ok(rt.cudaGraphInstantiate(graph, 0))
+        self._cuda_graphs = getattr(self, "_cuda_graphs", []) + [graph]  # keep alive
+        return exe
 
     def replay(self):
         """One rig-frame through the captured graph of the current parity."""
-        self._graphs[self.cur].replay()
+        if self._execs:
+            from cuda.bindings import runtime as rt
+            err = rt.cudaGraphLaunch(self._execs[self.cur],
+                                     torch.cuda.current_stream(self.dev).cuda_stream)
+            err = err[0] if isinstance(err, tuple) else err
+            if err != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"cudaGraphLaunch: {err}")
+        else:
+            self._graphs[self.cur].replay()
         self.cur = 1 - self.cur
 
     def table(self):

@@ -37,7 +37,8 @@ class Layout(ctypes.Structure):
 
 _SYMBOLS = ("v2d_pyramid_layout", "v2d_grid_k", "v2d_build_pyramid", "v2d_detect_gftt",
             "v2d_track_klt", "v2d_extract_patches", "v2d_suppress_mask", "v2d_track_survival",
-            "v2d_keyframe_decide", "v2d_refill_tracks", "v2d_strerror", "v2d_version")
+            "v2d_keyframe_decide", "v2d_refill_tracks", "v2d_strerror", "v2d_version",
+            "v2d_keyframe_decide_graph", "v2d_ring_tables")
 
 _lib = None
 
@@ -60,6 +61,8 @@ def load() -> ctypes.CDLL:
     L.v2d_suppress_mask.argtypes = [vp, vp, i, i, f, i, i, vp, i64, vp, vp]
     L.v2d_track_survival.argtypes = [vp, vp, i, i, vp, vp]
     L.v2d_keyframe_decide.argtypes = [vp, i, f, vp, vp, vp]
+    L.v2d_keyframe_decide_graph.argtypes = [vp, i, f, vp, vp, vp, ctypes.c_uint64, vp]
+    L.v2d_ring_tables.argtypes = [vp, i, i, vp, vp, vp, vp]
     L.v2d_refill_tracks.argtypes = [vp, vp, i, i, i, vp, i, i, vp, vp, vp, vp, vp, vp]
     L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
                                 vp, vp, vp, vp, vp, ctypes.c_uint, vp]
@@ -301,6 +304,24 @@ def keyframe_decide(counts, T, flag, totals=None):
     _need_cuda(counts, flag, totals)
     _check(load().v2d_keyframe_decide(_p(counts), counts.shape[0], float(T), _p(flag),
                                       _p(totals), _stream()), "keyframe_decide")
+
+
+def keyframe_decide_graph(counts, T, flag, totals=None, kf_count=None, cond_handle: int = 0):
+    """v2d_keyframe_decide_graph: the decision, the device keyframe counter and (inside a
+    captured graph) the conditional node's value."""
+    _need_cuda(counts, flag, totals, kf_count)
+    _check(load().v2d_keyframe_decide_graph(_p(counts), counts.shape[0], float(T), _p(flag),
+                                            _p(totals), _p(kf_count), int(cond_handle),
+                                            _stream()), "keyframe_decide_graph")
+
+
+def ring_tables(table, counter, cur, prev):
+    """v2d_ring_tables: rows counter and counter-1 (mod R) of the [R, C] int64 device
+    pointer table into cur / prev, then counter += 1 (all on the device)."""
+    R, C = table.shape
+    _need_cuda(table, counter, cur, prev)
+    _check(load().v2d_ring_tables(_p(table), R, C, _p(counter), _p(cur), _p(prev), _stream()),
+           "ring_tables")
 
 
 def refill_tracks(kp_xy, cell_count, grid_x, grid_y, k, flag, tracks, status, kf_member,

@@ -107,7 +107,7 @@ def test_validation_without_gpu(v2d):
     # empty batches are valid no-ops (no CUDA call is made for B == 0)
     assert L.v2d_build_pyramid(N, 64, 0, 64, 64, 3, N, N) == 0
     assert L.v2d_strerror(-2).decode().startswith("pitch")
-    assert L.v2d_version() == 200
+    assert L.v2d_version() == 201
     del args
 
 

@@ -83,6 +83,41 @@ def test_keyframe_tracker_graph_replay_matches_eager():
     for f in range(2, n):
         eager.step(table[f], table[f - 1])
     graph.capture(table, 2)
+    # the keyframe branch is a conditional (IF) graph node set by the decide kernel
+    assert graph.graph_kind == "conditional", getattr(graph, "graph_fallback_reason", "")
+    for f in range(2, n):
+        graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager.table(), graph.table()):
+        assert torch.equal(a, b)
+
+
+def test_keyframe_tracker_torch_graph_fallback_matches_eager():
+    """The torch.cuda.graph capture (no conditional node: the branch's kernels exit on
+    the device flag) gives the same tables as eager steps."""
+    from paper_2506_04359_b200 import vslam2d as v2d
+    from paper_2506_04359_b200.frontend import KeyframeTracker
+    wl = synth.WORKLOADS["c2"]
+    C, n = wl.cams, 10
+    st = synth.make_stream(wl, n, "cuda")
+    img = st.frames.stride(1) * st.frames.element_size()
+    cam = st.frames.stride(0) * st.frames.element_size()
+    t = torch.arange(n, device="cuda", dtype=torch.int64)[:, None]
+    c = torch.arange(C, device="cuda", dtype=torch.int64)[None, :]
+    table = (st.frames.data_ptr() + c * cam + t * img).contiguous()
+    cfg = v2d.FrontendConfig(W=wl.W, H=wl.H, levels=wl.levels, grid_x=wl.grid_x,
+                             grid_y=wl.grid_y, k=wl.k, K_min=wl.K_min, border=wl.border,
+                             win=wl.win, iters=wl.iters, eps=wl.eps, ncc_min=wl.ncc_min,
+                             min_eig=wl.min_eig)
+    eager = KeyframeTracker(cfg, C, "cuda", wl.pitch, T=0.9)
+    graph = KeyframeTracker(cfg, C, "cuda", wl.pitch, T=0.9)
+    for kt in (eager, graph):
+        kt.start(table[0])
+        kt.step(table[1], table[0])
+    for f in range(2, n):
+        eager.step(table[f], table[f - 1])
+    graph.capture(table, 2, conditional=False)
+    assert graph.graph_kind == "torch"
     for f in range(2, n):
         graph.replay()
     torch.cuda.synchronize()
