@@ -145,3 +145,7 @@ def test_keyframe_calls_validate_without_gpu(v2d):
     assert L.v2d_keyframe_decide(N, 0, f(0.7), N, N, N) == -1                   # null flag
     assert L.v2d_refill_tracks(N, N, 64, 32, 4, N, 0, 0, N, N, N, N, N, N) == -1  # > 1024 cells
     assert L.v2d_extract_patches(N, N, 64, 0, 64, 64, 2, N, 0, 8, N, N) == -1   # even patch
+    assert L.v2d_keyframe_decide_graph(N, 0, f(0.7), N, N, N, 0, N) == -1      # null flag
+    assert L.v2d_keyframe_decide_graph(N, 0, f(-1.0), N, N, N, 0, N) == -1     # T < 0
+    assert L.v2d_ring_tables(N, 0, 2, N, N, N, N) == -1                         # R < 1
+    assert L.v2d_ring_tables(N, 4, 2, N, N, N, N) == -1                         # null table

@@ -158,3 +158,30 @@ def test_overlap_streams_match_serial(name, F):
             assert torch.equal(a, b), s
     assert torch.equal(outs[0][1], outs[1][1])
     assert int((outs[0][1][..., 2] == 0).sum()) > 0
+
+
+def test_ring_tables_and_decide_graph_counter():
+    """v2d_ring_tables: rows t and t-1 (mod R, t = 0 wraps to row R-1) of the pointer
+    table, counter advanced; v2d_keyframe_decide_graph outside a graph (handle 0): the
+    Eq. 5 flag of v2d_keyframe_decide and kf_count += flag."""
+    from paper_2506_04359_b200 import vslam2d as v2d
+    R, C = 5, 3
+    table = torch.arange(R * C, dtype=torch.int64, device="cuda").view(R, C) * 16 + 4096
+    counter = torch.zeros((1,), dtype=torch.int64, device="cuda")
+    cur = torch.empty((C,), dtype=torch.int64, device="cuda")
+    prev = torch.empty_like(cur)
+    for t in range(2 * R + 1):
+        v2d.ring_tables(table, counter, cur, prev)
+        torch.cuda.synchronize()
+        assert torch.equal(cur, table[t % R]) and torch.equal(prev, table[(t - 1) % R]), t
+        assert int(counter.item()) == t + 1
+    counts = torch.tensor([[10, 6], [10, 8]], dtype=torch.int32, device="cuda")  # 14/20 = 0.7
+    flag = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    ref = torch.zeros_like(flag)
+    kf = torch.zeros((), dtype=torch.int64, device="cuda")
+    for T, want in ((0.71, 1), (0.7, 0), (0.69, 0), (1.0, 1)):
+        v2d.keyframe_decide_graph(counts, T, flag, None, kf)
+        v2d.keyframe_decide(counts, T, ref)
+        torch.cuda.synchronize()
+        assert int(flag.item()) == want == int(ref.item()), T
+    assert int(kf.item()) == 2
