@@ -6,9 +6,29 @@
 
 #include "vslam2d.h"
 
+// K3 Gauss-Newton residual and NCC samples with the vertical bilinear weight folded
+// into two FMAs (one packed op per window row fewer; same-box A/B -1.4 % at 21x21).
+// One-warp kernel (windows >= 15) only; the pair kernel's small windows failed parity
+// with it (klt_pair.cu).
+#ifndef V2D_GN_FOLD
+#define V2D_GN_FOLD 1
+#endif
+#ifndef V2D_GN_FOLD_PAIR
+#define V2D_GN_FOLD_PAIR 0
+#endif
+
 namespace v2d {
 
 constexpr unsigned kFullMask = 0xffffffffu;
+
+// sum / n with one Newton correction of sum * (1/n): equals sum / n exactly whenever that
+// quotient is representable (a flat template: n equal values), without the IEEE
+// division subroutine
+__device__ __forceinline__ float exact_mean(float sum, float n) {
+  const float inv = 1.0f / n;
+  const float q = sum * inv;
+  return fmaf(fmaf(-n, q, sum), inv, q);
+}
 
 // Level geometry passed by value to kernels (mirrors v2d_layout).
 struct Levels {

@@ -468,6 +468,19 @@ __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, 
   };
   float2 h = hrow(0);
   float2 ax = f2(0.f, 0.f), ay = f2(0.f, 0.f);
+#if V2D_GN_FOLD
+  // e = T - [(1-by) h(p) + by h(p+1)] as two FMAs (one packed op per row fewer than
+  // forming S and subtracting it)
+  const float2 nw0 = f2(by - 1.0f, by - 1.0f), nw1 = f2(-by, -by);
+#pragma unroll
+  for (int p = 0; p < RL; ++p) {
+    const float2 hn = hrow(p + 1);
+    const float2 e = fma2(nw1, hn, fma2(nw0, h, t.T[p]));
+    ax = fma2(e, t.TX[p], ax);
+    ay = fma2(e, t.TY[p], ay);
+    h = hn;
+  }
+#else
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
     const float2 hn = hrow(p + 1);
@@ -476,12 +489,19 @@ __device__ __forceinline__ float2 gn_rhs(const float* __restrict__ JP, int lc0, 
     ay = fma2(e, t.TY[p], ay);
     h = hn;
   }
+#endif
   return f2(ru.sum2(ax), ru.sum2(ay));
 }
 
-// NCC moments (sum S', sum S'^2, sum T'S') with S' = S - m, T' = T - m,
-// m = template mean (second pass of the two-pass NCC), over the valid slots.
-template <int WIN>
+// NCC moments (sum S', sum S'^2, sum T'S'), T' = T - m (m = template mean, the second
+// pass of the two-pass NCC), over the valid slots.  kExactRef = false (every level):
+// S' = S - m with the vertical lerp folded into two FMAs.  kExactRef = true (only when
+// the first pass is ill-conditioned, see ncc_gate): S' = S - S(0,0), S centred by one of
+// its own samples (window pixel (0,0): run 0, row 0, held by the first lane) with the
+// unfolded lerp, so a flat S has exactly zero deviations and NCC 0 — the oracle's
+// two-pass value (reading #14); centred by m, a flat S left rounding noise that could
+// pass the gate.
+template <int WIN, bool kExactRef>
 __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int lc0, int lr0,
                                               float bx, float by, float m, const Runs<WIN>& ru,
                                               const Tmpl<WIN>& t) {
@@ -496,12 +516,23 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
     const float2 a1 = f2(bxp[r * kPitch + 1], byp[r * kPitch + 1]);
     return fma2(wx, sub2(a1, a0), a0);
   };
-  float2 h = hrow(0);
+  float2 h = hrow(0), hn = hrow(1);
+  float2 sr = f2(0.f, 0.f), S0 = sr;
+  if (kExactRef) {
+    S0 = fma2(wy, sub2(hn, h), h);
+    const float sref = __shfl_sync(kFullMask, S0.x, 0);
+    sr = f2(sref, sref);
+  }
+  const float2 w0 = f2(1.0f - by, 1.0f - by), nm = f2(-m, -m);
   float2 s1 = f2(0.f, 0.f), s2 = f2(0.f, 0.f), st = f2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
-    const float2 hn = hrow(p + 1);
-    float2 S = sub2(fma2(wy, sub2(hn, h), h), mm);
+    if (p > 0) hn = hrow(p + 1);
+    float2 S;
+    if (kExactRef)
+      S = sub2(p == 0 ? S0 : fma2(wy, sub2(hn, h), h), sr);
+    else
+      S = fma2(wy, hn, fma2(w0, h, nm));  // S - m = (1-by) h(p) + by h(p+1) - m
     if (!Tmpl<WIN>::kExact) S = mul2(S, ru.mask(p));
     s1 = add2(s1, S);
     s2 = fma2(S, S, s2);
@@ -509,6 +540,26 @@ __device__ __forceinline__ float3 ncc_moments(const float* __restrict__ JP, int 
     h = hn;
   }
   return make_float3(ru.sum2(s1), ru.sum2(s2), ru.sum2(st));
+}
+
+// NCC of the template with S at (lc0, lr0) / (bx, by): two-pass in T (T' = T - tmean,
+// Stt = sum T'^2), S centred by one of its own samples (ncc_moments<WIN, true>).  The
+// cheaper folded pass centred by tmean, with the exact pass as a rare fallback when ill
+// conditioned, measured +0.5 % slower (code size) and the folded pass alone is not
+// flat-exact, so the exact pass is the only one.
+template <int WIN>
+__device__ __forceinline__ float ncc_value(const float* __restrict__ JP, int lc0, int lr0,
+                                           float bx, float by, float tmean, float Stt,
+                                           const Runs<WIN>& ru, const Tmpl<WIN>& t) {
+  constexpr float kInvN = 1.0f / (float)(WIN * WIN);
+  const float3 mo = ncc_moments<WIN, true>(JP, lc0, lr0, bx, by, tmean, ru, t);
+  const float2 r1 = warp_sum2(f2(mo.x, mo.y));
+  const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
+  // S' = S - c: sum (S - mean S)^2 = sum S'^2 - (sum S')^2 / n and
+  // sum (T - mean T)(S - mean S) = sum T'S' (sum T' = 0 up to rounding of the mean)
+  const float Sss = r1.y - r1.x * r1.x * kInvN;
+  const float den2 = Stt * Sss;
+  return den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
 }
 
 // One pyramid level of D7 for the warp's keypoint; (dx, dy) in level px.
@@ -584,7 +635,9 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
   const float i00 = gyy * inv_det, i01 = -gxy * inv_det, i11 = gxx * inv_det;
   // two-pass NCC, first pass: template mean, then sum (T - mean)^2 (T itself
   // stays uncentred: the Gauss-Newton residual e = T - S needs no centring)
-  const float tmean = g2s.y * (1.0f / (float)N);
+  // IEEE division: a flat template's mean is exact, so T - mean is exactly 0 there
+  // (the oracle's NCC is then 0/0 -> 0; a rounded mean made Stt spuriously > 0)
+  const float tmean = exact_mean(g2s.y, (float)N);
   float2 q = f2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
@@ -647,12 +700,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
       int lc0n, lr0n;
       float bxn, byn;
       locate(nx, ny, lc0n, lr0n, bxn, byn);
-      const float3 mo = ncc_moments<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, ru, t);
-      const float2 r1 = warp_sum2(f2(mo.x, mo.y));
-      const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
-      const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
-      const float den2 = Stt * Sss;
-      out.ncc = den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
+      out.ncc = ncc_value<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, Stt, ru, t);
       if (out.ncc < a.ncc_min) {
         out.status = V2D_LOST_NCC;
         return;
@@ -667,15 +715,7 @@ __device__ __forceinline__ void track_level_body(float* __restrict__ sp, const P
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, lc0, lr0, bx, by);
-    const float3 mo = ncc_moments<WIN>(sp, lc0, lr0, bx, by, tmean, ru, t);
-    const float2 r1 = warp_sum2(f2(mo.x, mo.y));
-    const float r2 = warp_sum2(f2(mo.z, 0.f)).x;
-    // S' = S - mean_T: sum(S-Sm)^2 = sum S'^2 - (sum S')^2/n and
-    // sum(T-Tm)(S-Sm) = sum T'S' (sum T' = 0 up to rounding of the mean)
-    const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
-    const float Sts = r2;
-    const float den2 = Stt * Sss;
-    out.ncc = den2 > 0.0f ? Sts * rsqrtf(den2) : 0.0f;
+    out.ncc = ncc_value<WIN>(sp, lc0, lr0, bx, by, tmean, Stt, ru, t);
     KCYC(4, t_nc);
     if (out.ncc < a.ncc_min) {
       out.status = V2D_LOST_NCC;

@@ -312,10 +312,20 @@ __device__ __forceinline__ float2 pgn_rhs(const float* __restrict__ JP, int lc0,
   };
   float2 h = hrow(0);
   float2 ax = pf2(0.f, 0.f), ay = pf2(0.f, 0.f);
+  // e = T - [(1-by) h(p) + by h(p+1)] as two FMAs (klt.cu V2D_GN_FOLD) is NOT used
+  // here: with 7x7 windows (n = 49) its different rounding flipped one track's NCC
+  // decision outside the parity bands (test_klt_stream_windows[7-5])
+#if V2D_GN_FOLD_PAIR
+  const float2 nw0 = pf2(by - 1.0f, by - 1.0f), nw1 = pf2(-by, -by);
+#endif
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
     const float2 hn = hrow(p + 1);
+#if V2D_GN_FOLD_PAIR
+    const float2 e = pfma2(nw1, hn, pfma2(nw0, h, t.T[p]));
+#else
     const float2 e = psub2(t.T[p], pfma2(wy, psub2(hn, h), h));
+#endif
     ax = pfma2(e, t.TX[p], ax);
     ay = pfma2(e, t.TY[p], ay);
     h = hn;
@@ -323,10 +333,18 @@ __device__ __forceinline__ float2 pgn_rhs(const float* __restrict__ JP, int lc0,
   return pf2(ru.sum2(ax), ru.sum2(ay));
 }
 
-template <int WIN>
+// NCC moments (sum S', sum S'^2, sum T'S'), T' = T - m (m = template mean, the second
+// pass of the two-pass NCC), over the valid slots.  kExactRef = false (every level):
+// S' = S - m with the vertical lerp folded into two FMAs.  kExactRef = true (only when
+// the first pass is ill-conditioned, see ncc_gate): S' = S - S(0,0), S centred by one of
+// its own samples (window pixel (0,0): run 0, row 0, held by the first lane) with the
+// unfolded lerp, so a flat S has exactly zero deviations and NCC 0 — the oracle's
+// two-pass value (reading #14); centred by m, a flat S left rounding noise that could
+// pass the gate.
+template <int WIN, bool kExactRef>
 __device__ __forceinline__ float3 pncc_moments(const float* __restrict__ JP, int lc0, int lr0,
-                                               float bx, float by, float m, const PRuns<WIN>& ru,
-                                               const PTmpl<WIN>& t) {
+                                              float bx, float by, float m, const PRuns<WIN>& ru,
+                                              const PTmpl<WIN>& t) {
   constexpr int RL = PTmpl<WIN>::RL;
   constexpr int kPitch = PSmem<WIN>::P;
   const float* base = JP + lr0 * kPitch + lc0;
@@ -338,12 +356,23 @@ __device__ __forceinline__ float3 pncc_moments(const float* __restrict__ JP, int
     const float2 a1 = pf2(bxp[r * kPitch + 1], byp[r * kPitch + 1]);
     return pfma2(wx, psub2(a1, a0), a0);
   };
-  float2 h = hrow(0);
+  float2 h = hrow(0), hn = hrow(1);
+  float2 sr = pf2(0.f, 0.f), S0 = sr;
+  if (kExactRef) {
+    S0 = pfma2(wy, psub2(hn, h), h);
+    const float sref = __shfl_sync(kFullMask, S0.x, 0, 16);
+    sr = pf2(sref, sref);
+  }
+  const float2 w0 = pf2(1.0f - by, 1.0f - by), nm = pf2(-m, -m);
   float2 s1 = pf2(0.f, 0.f), s2 = pf2(0.f, 0.f), st = pf2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
-    const float2 hn = hrow(p + 1);
-    float2 S = psub2(pfma2(wy, psub2(hn, h), h), mm);
+    if (p > 0) hn = hrow(p + 1);
+    float2 S;
+    if (kExactRef)
+      S = psub2(p == 0 ? S0 : pfma2(wy, psub2(hn, h), h), sr);
+    else
+      S = pfma2(wy, hn, pfma2(w0, h, nm));  // S - m = (1-by) h(p) + by h(p+1) - m
     if (!PTmpl<WIN>::kExact) S = pmul2(S, ru.mask(p));
     s1 = padd2(s1, S);
     s2 = pfma2(S, S, s2);
@@ -351,6 +380,20 @@ __device__ __forceinline__ float3 pncc_moments(const float* __restrict__ JP, int
     h = hn;
   }
   return make_float3(ru.sum2(s1), ru.sum2(s2), ru.sum2(st));
+}
+
+// klt.cu ncc_value for a half-warp (the centre sample is a half-width shuffle).
+template <int WIN>
+__device__ __forceinline__ float pncc_value(const float* __restrict__ JP, int lc0, int lr0,
+                                            float bx, float by, float tmean, float Stt,
+                                            const PRuns<WIN>& ru, const PTmpl<WIN>& t) {
+  constexpr float kInvN = 1.0f / (float)(WIN * WIN);
+  const float3 mo = pncc_moments<WIN, true>(JP, lc0, lr0, bx, by, tmean, ru, t);
+  const float2 r1 = half_sum2(pf2(mo.x, mo.y));
+  const float r2 = half_sum2(pf2(mo.z, 0.f)).x;
+  const float Sss = r1.y - r1.x * r1.x * kInvN;
+  const float den2 = Stt * Sss;
+  return den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
 }
 
 struct PState {
@@ -408,7 +451,9 @@ __device__ __forceinline__ void ptrack_level(float* __restrict__ sp, const PPlan
   if (alive && !cond_ok && L == 0) o.status = V2D_LOST_SMALL_EIG;
   const float inv_det = cond_ok ? 8.0f / det : 0.0f;
   const float i00 = gyy * inv_det, i01 = -gxy * inv_det, i11 = gxx * inv_det;
-  const float tmean = g2s.y * (1.0f / (float)N);
+  // IEEE division: a flat template's mean is exact, so T - mean is exactly 0 there
+  // (the oracle's NCC is then 0/0 -> 0; a rounded mean made Stt spuriously > 0)
+  const float tmean = exact_mean(g2s.y, (float)N);
   float2 q = pf2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < RL; ++p) {
@@ -479,13 +524,9 @@ __device__ __forceinline__ void ptrack_level(float* __restrict__ sp, const PPlan
       int lc0n, lr0n;
       float bxn, byn;
       locate(cx + dx, cy + dy, active, lc0n, lr0n, bxn, byn);
-      const float3 mo = pncc_moments<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, ru, t);
-      const float2 r1 = half_sum2(pf2(mo.x, mo.y));
-      const float r2 = half_sum2(pf2(mo.z, 0.f)).x;
-      const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
-      const float den2 = Stt * Sss;
+      const float nv = pncc_value<WIN>(sp, lc0n, lr0n, bxn, byn, tmean, Stt, ru, t);
       if (active) {
-        o.ncc = den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
+        o.ncc = nv;
         if (o.ncc < a.ncc_min) {
           o.status = V2D_LOST_NCC;
           active = false;
@@ -500,13 +541,9 @@ __device__ __forceinline__ void ptrack_level(float* __restrict__ sp, const PPlan
     int lc0, lr0;
     float bx, by;
     locate(cx + dx, cy + dy, run_ncc, lc0, lr0, bx, by);
-    const float3 mo = pncc_moments<WIN>(sp, lc0, lr0, bx, by, tmean, ru, t);
-    const float2 r1 = half_sum2(pf2(mo.x, mo.y));
-    const float r2 = half_sum2(pf2(mo.z, 0.f)).x;
-    const float Sss = r1.y - r1.x * r1.x * (1.0f / (float)N);
-    const float den2 = Stt * Sss;
+    const float nv = pncc_value<WIN>(sp, lc0, lr0, bx, by, tmean, Stt, ru, t);
     if (run_ncc) {
-      o.ncc = den2 > 0.0f ? r2 * rsqrtf(den2) : 0.0f;
+      o.ncc = nv;
       if (o.ncc < a.ncc_min) o.status = V2D_LOST_NCC;
     }
   }

@@ -26,7 +26,10 @@ def _dev(frames):
     return t.cuda()
 
 
-@pytest.mark.parametrize("case", range(int(os.environ.get("V2D_FUZZ_CASES", "24"))))
+# 200 seeded cases by default (cases 100 and 169 are the flat-window NCC regressions:
+# a flat S or T must give NCC 0 as in the oracle).  V2D_FUZZ_CASES=1000 runs more;
+# DESIGN.md §2 lists the 4 of 1000 that fail (unconverged tracks at the iteration cap).
+@pytest.mark.parametrize("case", range(int(os.environ.get("V2D_FUZZ_CASES", "200"))))
 def test_fuzz_detect_and_track(case):
     rng = np.random.default_rng(9000 + case)
     win = int(rng.choice([5, 7, 9, 11, 13, 15, 17, 19, 21]))
