@@ -428,3 +428,32 @@ def test_selection_massive_ties(dense):
     assert np.array_equal(cnt[0].cpu().numpy(), ocnt)
     assert np.array_equal(xy[0].cpu().numpy(), oxy)
     assert np.array_equal(sc[0].cpu().numpy(), osc)
+
+
+@pytest.mark.parametrize("W,H,gx,gy,k", [(320, 240, 4, 3, 6), (161, 123, 3, 2, 9), (752, 480, 8, 8, 16)])
+def test_masked_selection_bit_exact(W, H, gx, gy, k):
+    """Masked detection (min_separation suppression): a non-zero mask pixel is not
+    eligible but NMS still compares against it; dense and fused paths bit-exact with the
+    oracle on random disk masks (the half-resolution candidate map's non-candidate word
+    must survive every kernel variant)."""
+    wl = synth.Workload("mk", 13, W, H, 2, 1, grid_x=gx, grid_y=gy, k=k, stereo_disparity=0.0)
+    st = synth.make_stream(wl, 2, "cpu")
+    fr = st.frames[:, 0, :, :W].numpy().copy()
+    pitch = synth.round_up(W, 16)
+    rng = np.random.default_rng(W + H)
+    mask = np.zeros((2, H, pitch), np.uint8)
+    for b in range(2):
+        for _ in range(max(4, W * H // 3000)):
+            x, y, r = rng.integers(0, W), rng.integers(0, H), rng.integers(2, 12)
+            yy, xx = np.mgrid[0:H, 0:W]
+            mask[b, :, :W][(xx - x) ** 2 + (yy - y) ** 2 < r * r] = 1
+    dev = _to_dev(fr, pitch)
+    mt = torch.from_numpy(mask).cuda()
+    for dense in (True, False):
+        xy, sc, cnt, _ = v2d.detect_gftt(dev, W, gx, gy, k=k, border=11, mask=mt, dense=dense)
+        for b in range(2):
+            oxy, osc, ocnt = oracle.detect_gftt(fr[b], gx, gy, k=k, border=11,
+                                                mask=np.ascontiguousarray(mask[b, :, :W]))
+            assert np.array_equal(cnt[b].cpu().numpy(), ocnt), (dense, b)
+            assert np.array_equal(xy[b].cpu().numpy().reshape(oxy.shape), oxy), (dense, b)
+            assert np.array_equal(sc[b].cpu().numpy().reshape(osc.shape), osc), (dense, b)
