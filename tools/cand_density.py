@@ -1,7 +1,8 @@
 """Probe: NMS candidates per grid cell on the bench workloads (input for the K2 pass B
 design).  Runs detection through the C-ABI with a caller-owned
-workspace and counts the pass-A map's candidates (ws >= 0) inside each cell's
-eligible region.  usage (GPU box): python tools/cand_density.py [c2 c3 c4 c5]"""
+workspace and counts the pass-A map's candidates inside each cell's eligible region
+(nms = 1: the half-resolution map, one int32 word per pixel pair, bits(R) | dx << 31 or
+all ones; decoded back to a per-pixel candidate image here).  usage (GPU box): python tools/cand_density.py [c2 c3 c4 c5]"""
 import json
 import sys
 
@@ -25,7 +26,13 @@ for name in sys.argv[1:] or ["c2", "c3", "c4", "c5"]:
     v.detect_gftt_ptrs(v.ptrs_of(fr), fr.stride(1), B, wl.W, wl.H, wl.grid_x, wl.grid_y, wl.k,
                        wl.K_min, 0.0, wl.border, 1, xy, sc, cnt, None, None, None, ws)
     torch.cuda.synchronize()
-    c = (ws[:, :, : wl.W] >= 0)
+    words = ws.view(torch.int32)[:, :, : v.workspace_pitch(wl.W) // 2]  # [B, H, pairs]
+    valid = words != -1
+    dx = (words < 0) & valid  # bit 31 set on a candidate = right pixel of the pair
+    c = torch.zeros((B, wl.H, 2 * words.shape[2]), dtype=torch.bool, device="cuda")
+    c[:, :, 0::2] = valid & ~dx
+    c[:, :, 1::2] = dx
+    c = c[:, :, : wl.W]
     per = []
     for cy in range(wl.grid_y):
         y0 = max(cy * wl.H // wl.grid_y, wl.border)
