@@ -26,7 +26,8 @@ for name in sys.argv[1:] or ["c2", "c3", "c4", "c5"]:
     v.detect_gftt_ptrs(v.ptrs_of(fr), fr.stride(1), B, wl.W, wl.H, wl.grid_x, wl.grid_y, wl.k,
                        wl.K_min, 0.0, wl.border, 1, xy, sc, cnt, None, None, None, ws)
     torch.cuda.synchronize()
-    words = ws.view(torch.int32)[:, :, : v.workspace_pitch(wl.W) // 2]  # [B, H, pairs]
+    wp = v.workspace_pitch(wl.W) // 2  # words per half-map row, rows packed from the start
+    words = ws.view(torch.int32).reshape(-1)[: B * wl.H * wp].view(B, wl.H, wp)
     valid = words != -1
     dx = (words < 0) & valid  # bit 31 set on a candidate = right pixel of the pair
     c = torch.zeros((B, wl.H, 2 * words.shape[2]), dtype=torch.bool, device="cuda")
