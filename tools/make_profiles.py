@@ -17,7 +17,7 @@ GO = os.path.join(ROOT, "gpurun_out")
 PR = os.path.join(ROOT, "profiles")
 tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
 cfg = sys.argv[2] if len(sys.argv) > 2 else "c5"
-KERNELS = ("pyramid_kernel", "gftt_dense_kernel", "gftt_select_kernel", "klt_kernel")
+KERNELS = ("pyramid_kernel", "gftt_dense_kernel", "gftt_select", "klt_kernel")
 
 # ---- launch list -----------------------------------------------------------
 src = os.path.join(GO, f"{tag}_launches_{cfg}.csv")
@@ -73,7 +73,7 @@ def dram_bytes(rep):
 tr = {}
 for k, key in (("klt_kernel", "klt"), ("pyramid_kernel", "pyramid"),
                ("gftt_dense_kernel", "gftt_dense_kernel"),
-               ("gftt_select_kernel", "gftt_select_kernel")):
+               ("gftt_select", "gftt_select_kernel")):
     rep = os.path.join(GO, f"{tag}_full_{cfg}_{k}.ncu-rep")
     if os.path.exists(rep):
         tr[key] = dram_bytes(rep)
