@@ -630,8 +630,8 @@ def main():
                                  f"{ms_max / args.steps:.3f} ms"
                                  if e2e["h2d_copy_ms"] >= 0.95 * ms_max / args.steps else
                                  "kernels"),
-                       "api": "frontend.HostStream (H2D / D2H on a copy stream, "
-                              "overlapping the kernels of neighbouring steps)"}
+                       "api": "frontend.HostStream (H2D on a copy stream, D2H on a read-back "
+                              "stream, both overlapping the kernels of neighbouring steps)"}
     if world > 1:
         line["shard_check"] = verify_shards(wl, lay, world, rank, fe, sched, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -148,9 +148,11 @@ class HostStream:
         copy stream : wait kernels(s-1) -> H2D frames(s+1) into slot (s+1) % 3
         main stream : wait H2D(s) -> the three launches of step s -> snapshot
                       (D2D) of the step's keypoints, positions and statuses
-        copy stream : wait kernels(s) -> D2H of the snapshot into pinned buffers
+        read stream : wait kernels(s) -> D2H of the snapshot into pinned buffers
 
-    so uploads and read-backs overlap the kernels.  Three device frame slots are
+    so uploads and read-backs overlap the kernels.  The read-backs have their own
+    stream (the other copy direction): on one stream a read-back waiting for step s's
+    kernels held back the upload of step s+2 queued behind it.  Three device frame slots are
     needed because step s reads its own frames and the last frame of step s-1;
     two snapshot/host result sets let read-back s overlap kernels s+1."""
 
@@ -166,6 +168,7 @@ class HostStream:
         # last frame of the slot before
         self.prev_t = [v2d.ptr_table(addr[(i - 1) % 3][-C:] + addr[i][:-C], d) for i in range(3)]
         self.copy = torch.cuda.Stream(device=d)
+        self.read = torch.cuda.Stream(device=d)
         self.ev_in = [torch.cuda.Event() for _ in range(3)]
         self.ev_done = [torch.cuda.Event() for _ in range(3)]
         self.ev_out = [torch.cuda.Event() for _ in range(2)]
@@ -215,12 +218,12 @@ class HostStream:
     def download(self, s: int):
         """Enqueue the D2H read-back of step s's results into host set s % 2."""
         j = s % 2
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(self.ev_done[s % 3])
+        with torch.cuda.stream(self.read):
+            self.read.wait_event(self.ev_done[s % 3])
             self.host_kp[j].copy_(self.snap_kp[j], non_blocking=True)
             self.host_pos[j].copy_(self.snap_pos[j], non_blocking=True)
             self.host_st[j].copy_(self.snap_st[j], non_blocking=True)
-            self.ev_out[j].record(self.copy)
+            self.ev_out[j].record(self.read)
 
     def results(self, s: int):
         """Host (kp_xy, pos, status) of step s once ev_out[s % 2] has completed."""
@@ -231,6 +234,7 @@ class HostStream:
     def finish(self):
         """Make the main stream wait for all pending copies."""
         torch.cuda.current_stream().wait_stream(self.copy)
+        torch.cuda.current_stream().wait_stream(self.read)
 
 
 class RingSchedule:
