@@ -20,10 +20,16 @@ namespace v2d {
 namespace {
 
 constexpr int kWarps = 8;
-constexpr int kBudget = 1024;  // staged pixels per warp (4 KB of shared memory)
+#ifndef V2D_PATCH_BUDGET
+#define V2D_PATCH_BUDGET 512  // 9x9 x 5 levels still one batch; 16 KB per CTA
+#endif
+#ifndef V2D_PATCH_MINB
+#define V2D_PATCH_MINB 8  // 64 warps per SM (32 registers): -7 % at c5 (same-box A/B)
+#endif
+constexpr int kBudget = V2D_PATCH_BUDGET;  // staged pixels per warp (2 KB of shared memory)
 
 template <int PATCH>  // compile-time patch edge
-__global__ void __launch_bounds__(32 * kWarps)
+__global__ void __launch_bounds__(32 * kWarps, V2D_PATCH_MINB)
 patches_kernel(const uint8_t* const* __restrict__ l0_ptrs, const float* const* __restrict__ pyr_ptrs,
                int64_t l0_pitch, int B, Levels lv, const float* __restrict__ pts, int P,
                float* __restrict__ out) {
