@@ -200,6 +200,18 @@ int v2d_keyframe_decide_graph(const int32_t* counts, int n, float T, int32_t* fl
                               int64_t* totals, int64_t* kf_count, uint64_t cond_handle,
                               v2d_stream_t stream);
 
+/* v2d_track_survival + v2d_keyframe_decide_graph over all B images in ONE launch (the f1
+ * loop is launch-bound): counts[b] as v2d_track_survival, then the last block to finish
+ * takes the rig-wide decision into *flag (totals, kf_count, cond_handle as in
+ * v2d_keyframe_decide_graph).  done: device uint32[1], 0 before the first call; the
+ * launch leaves it 0 (one launch at a time per `done`).  Single-process rigs; with a
+ * multi-GPU group use v2d_track_survival, an all-reduce and v2d_keyframe_decide.
+ * V2D_EINVAL: B < 1 or > 65535, null counts/flag/done, T < 0 or NaN. */
+int v2d_survival_decide(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                        int32_t* counts, float T, int32_t* flag, int64_t* totals,
+                        int64_t* kf_count, uint64_t cond_handle, uint32_t* done,
+                        v2d_stream_t stream);
+
 /* Frame tables of a captured streaming loop (the graph replays with no host work):
  * t = *counter; cur[c] = table[t mod R][c], prev[c] = table[(t-1) mod R][c] for
  * c < C (device pointers as int64; table: device int64 [R][C]); then *counter = t+1.

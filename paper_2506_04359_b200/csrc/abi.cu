@@ -183,6 +183,19 @@ int v2d_keyframe_decide_graph(const int32_t* counts, int n, float T, int32_t* fl
                             reinterpret_cast<cudaStream_t>(stream));
 }
 
+int v2d_survival_decide(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                        int32_t* counts, float T, int32_t* flag, int64_t* totals,
+                        int64_t* kf_count, uint64_t cond_handle, uint32_t* done,
+                        v2d_stream_t stream) {
+  if (B < 1 || B > 65535 || P < 0 || !counts || !flag || !done || !(T >= 0.0f) ||
+      (P > 0 && (!status || !kf_member)))
+    return V2D_EINVAL;
+  return v2d::launch_survival_decide(status, kf_member, B, P, counts, T, flag, totals, kf_count,
+                                     (unsigned long long)cond_handle,
+                                     reinterpret_cast<unsigned*>(done),
+                                     reinterpret_cast<cudaStream_t>(stream));
+}
+
 int v2d_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
                     int64_t* prev, v2d_stream_t stream) {
   if (R < 1 || C < 1 || C > 65535 || !table || !counter || !cur || !prev) return V2D_EINVAL;

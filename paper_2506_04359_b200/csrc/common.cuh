@@ -88,6 +88,10 @@ int launch_survival(const uint8_t* status, const uint8_t* kf_member, int B, int 
                     cudaStream_t st);
 int launch_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
                   int64_t* kf_count, unsigned long long cond, cudaStream_t st);
+int launch_survival_decide(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                           int32_t* counts, float T, int32_t* flag, int64_t* totals,
+                           int64_t* kf_count, unsigned long long cond, unsigned* done,
+                           cudaStream_t st);
 int launch_ring_tables(const int64_t* table, int R, int C, int64_t* counter, int64_t* cur,
                        int64_t* prev, cudaStream_t st);
 int launch_refill(const float* kp_xy, const int32_t* cell_count, int cells, int k,

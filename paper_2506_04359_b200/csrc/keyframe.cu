@@ -119,6 +119,64 @@ __global__ void decide_kernel(const int32_t* __restrict__ counts, int n, float T
   if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, (unsigned)f);
 }
 
+// survival_kernel + decide_kernel in one launch (the f1 loop is launch-bound): each CTA
+// counts one image, publishes its counts, and the last CTA to finish (device counter
+// `done`, left at 0 again) takes the rig-wide Eq. 5 decision exactly as decide_kernel.
+__global__ void survival_decide_kernel(const uint8_t* __restrict__ status,
+                                       const uint8_t* __restrict__ kf_member, int P,
+                                       int32_t* __restrict__ counts, float T,
+                                       int32_t* __restrict__ flag, int64_t* __restrict__ totals,
+                                       int64_t* __restrict__ kf_count, unsigned long long cond,
+                                       unsigned* __restrict__ done) {
+  const int b = blockIdx.x, n = gridDim.x;
+  int nk = 0, ns = 0;
+  for (int p = threadIdx.x; p < P; p += kT) {
+    const int64_t s = (int64_t)b * P + p;
+    const int k = kf_member[s] != 0;
+    nk += k;
+    ns += k & (status[s] == V2D_TRACKED);
+  }
+  __shared__ int sk[kT / 32], ss[kT / 32];
+  __shared__ bool last;
+  for (int o = 16; o > 0; o >>= 1) {
+    nk += __shfl_xor_sync(kFullMask, nk, o);
+    ns += __shfl_xor_sync(kFullMask, ns, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sk[threadIdx.x >> 5] = nk;
+    ss[threadIdx.x >> 5] = ns;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, c = 0;
+    for (int w = 0; w < kT / 32; ++w) {
+      a += sk[w];
+      c += ss[w];
+    }
+    counts[2 * b] = a;
+    counts[2 * b + 1] = c;
+    __threadfence();  // this image's counts are visible before it is counted as done
+    last = atomicAdd(done, 1u) == (unsigned)(n - 1);
+  }
+  __syncthreads();
+  if (!last || threadIdx.x != 0) return;
+  __threadfence();
+  int64_t tk = 0, ts = 0;
+  for (int i = 0; i < n; ++i) {
+    tk += ((volatile int32_t*)counts)[2 * i];
+    ts += ((volatile int32_t*)counts)[2 * i + 1];
+  }
+  const int f = (tk == 0 || (double)ts < (double)T * (double)tk) ? 1 : 0;
+  flag[0] = f;
+  if (totals) {
+    totals[0] = tk;
+    totals[1] = ts;
+  }
+  if (kf_count) kf_count[0] += f;
+  *done = 0u;  // ready for the next frame (the next launch is stream-ordered after this one)
+  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, (unsigned)f);
+}
+
 // Frame tables of a captured streaming loop: t = *counter, cur/prev = rows t and t-1
 // (mod R) of the [R][C] device-pointer table, then *counter = t + 1.
 __global__ void ring_tables_kernel(const int64_t* __restrict__ table, int R, int C,
@@ -238,6 +296,15 @@ int launch_survival(const uint8_t* status, const uint8_t* kf_member, int B, int 
 int launch_decide(const int32_t* counts, int n, float T, int32_t* flag, int64_t* totals,
                   int64_t* kf_count, unsigned long long cond, cudaStream_t st) {
   decide_kernel<<<1, 32, 0, st>>>(counts, n, T, flag, totals, kf_count, cond);
+  return cudaGetLastError() == cudaSuccess ? V2D_OK : V2D_ECUDA;
+}
+
+int launch_survival_decide(const uint8_t* status, const uint8_t* kf_member, int B, int P,
+                           int32_t* counts, float T, int32_t* flag, int64_t* totals,
+                           int64_t* kf_count, unsigned long long cond, unsigned* done,
+                           cudaStream_t st) {
+  survival_decide_kernel<<<B, kT, 0, st>>>(status, kf_member, P, counts, T, flag, totals,
+                                           kf_count, cond, done);
   return cudaGetLastError() == cudaSuccess ? V2D_OK : V2D_ECUDA;
 }
 

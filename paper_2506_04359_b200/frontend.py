@@ -284,9 +284,10 @@ class KeyframeTracker:
         v2d_build_pyramid   (frame t)
         v2d_track_klt       (live tracks t-1 -> t; lost slots are SKIPPED because the
                              status table is fed back as in_status: lost is terminal)
-        v2d_track_survival  (per camera |S_kf|, |S_curr ∩ S_kf|)
-        v2d_keyframe_decide (rig-wide Eq. 5 into a device flag; multi-GPU: the totals
-                             are all-reduced first)
+        v2d_survival_decide (per camera |S_kf|, |S_curr ∩ S_kf| and the rig-wide Eq. 5
+                             decision into a device flag, one launch; multi-GPU:
+                             v2d_track_survival, an all-reduce of the totals, then
+                             v2d_keyframe_decide)
         -- device-flag gated, no host round trip --
         v2d_suppress_mask   (min_separation disks around live tracks)
         v2d_detect_gftt     (masked grid top-k)
@@ -325,6 +326,7 @@ class KeyframeTracker:
         self.ncc = torch.zeros((C, P), device=d)
         self.iters = torch.zeros((C, P), dtype=torch.int32, device=d)
         self.kf_count = torch.zeros((), dtype=torch.int64, device=d)  # keyframes so far
+        self.done = torch.zeros((1,), dtype=torch.int32, device=d)    # survival_decide counter
         self.cur = 0
 
     def _keyframe_branch(self, l0_ptrs, j):
@@ -354,6 +356,12 @@ class KeyframeTracker:
                            C, c.W, c.H, c.levels, self.tracks[i], None, self.status[i], P, c.win,
                            c.iters, c.eps, c.ncc_min, c.min_eig, self.tracks[j], self.status[j],
                            self.ncc, self.iters, c.klt_flags)
+        if self.group is None:  # one launch: counts and the rig-wide Eq. 5 decision
+            v2d.survival_decide(self.status[j], self.kf_member, self.counts, self.T, self.flag,
+                                self.done, self.totals)
+            self._keyframe_branch(l0_ptrs, j)
+            self.cur = j
+            return
         v2d.track_survival(self.status[j], self.kf_member, self.counts)
         if self.group is not None:
             from .shard import all_reduce_sum_
@@ -376,9 +384,8 @@ class KeyframeTracker:
                            C, c.W, c.H, c.levels, self.tracks[i], None, self.status[i], P, c.win,
                            c.iters, c.eps, c.ncc_min, c.min_eig, self.tracks[j], self.status[j],
                            self.ncc, self.iters, c.klt_flags)
-        v2d.track_survival(self.status[j], self.kf_member, self.counts)
-        v2d.keyframe_decide_graph(self.counts, self.T, self.flag, self.totals, self.kf_count,
-                                  cond_handle)
+        v2d.survival_decide(self.status[j], self.kf_member, self.counts, self.T, self.flag,
+                            self.done, self.totals, self.kf_count, cond_handle)
 
     def capture(self, frame_table: torch.Tensor, next_frame: int, conditional: bool = True):
         """Record the per-frame step as CUDA graphs (the loop is launch-bound: 8+

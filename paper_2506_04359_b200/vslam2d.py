@@ -38,7 +38,7 @@ class Layout(ctypes.Structure):
 _SYMBOLS = ("v2d_pyramid_layout", "v2d_grid_k", "v2d_build_pyramid", "v2d_detect_gftt",
             "v2d_track_klt", "v2d_extract_patches", "v2d_suppress_mask", "v2d_track_survival",
             "v2d_keyframe_decide", "v2d_refill_tracks", "v2d_strerror", "v2d_version",
-            "v2d_keyframe_decide_graph", "v2d_ring_tables")
+            "v2d_keyframe_decide_graph", "v2d_ring_tables", "v2d_survival_decide")
 
 _lib = None
 
@@ -63,6 +63,7 @@ def load() -> ctypes.CDLL:
     L.v2d_keyframe_decide.argtypes = [vp, i, f, vp, vp, vp]
     L.v2d_keyframe_decide_graph.argtypes = [vp, i, f, vp, vp, vp, ctypes.c_uint64, vp]
     L.v2d_ring_tables.argtypes = [vp, i, i, vp, vp, vp, vp]
+    L.v2d_survival_decide.argtypes = [vp, vp, i, i, vp, f, vp, vp, vp, ctypes.c_uint64, vp, vp]
     L.v2d_refill_tracks.argtypes = [vp, vp, i, i, i, vp, i, i, vp, vp, vp, vp, vp, vp]
     L.v2d_track_klt.argtypes = [vp, vp, vp, vp, i64, i, i, i, i, vp, vp, vp, i, i, i, f, f, f,
                                 vp, vp, vp, vp, vp, ctypes.c_uint, vp]
@@ -313,6 +314,17 @@ def keyframe_decide_graph(counts, T, flag, totals=None, kf_count=None, cond_hand
     _check(load().v2d_keyframe_decide_graph(_p(counts), counts.shape[0], float(T), _p(flag),
                                             _p(totals), _p(kf_count), int(cond_handle),
                                             _stream()), "keyframe_decide_graph")
+
+
+def survival_decide(status, kf_member, counts, T, flag, done, totals=None, kf_count=None,
+                    cond_handle: int = 0):
+    """v2d_survival_decide: per-image survival counts and the rig-wide Eq. 5 decision in
+    one launch (done: int32/uint32 [1] device counter, zero)."""
+    B, P = status.shape
+    _need_cuda(status, kf_member, counts, flag, done, totals, kf_count)
+    _check(load().v2d_survival_decide(_p(status), _p(kf_member), B, P, _p(counts), float(T),
+                                      _p(flag), _p(totals), _p(kf_count), int(cond_handle),
+                                      _p(done), _stream()), "survival_decide")
 
 
 def ring_tables(table, counter, cur, prev):

@@ -185,3 +185,34 @@ def test_ring_tables_and_decide_graph_counter():
         torch.cuda.synchronize()
         assert int(flag.item()) == want == int(ref.item()), T
     assert int(kf.item()) == 2
+
+
+def test_survival_decide_matches_survival_then_decide():
+    """v2d_survival_decide (one launch, last-block decision) == v2d_track_survival +
+    v2d_keyframe_decide on random tables, repeatedly (the done counter returns to 0)."""
+    from paper_2506_04359_b200 import vslam2d as v2d
+    g = torch.Generator(device="cpu").manual_seed(3)
+    done = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    kf = torch.zeros((), dtype=torch.int64, device="cuda")
+    n_kf = 0
+    for it in range(12):
+        B, P = [(1, 5), (7, 300), (32, 2048), (3, 1)][it % 4]
+        status = torch.randint(0, 5, (B, P), generator=g, dtype=torch.uint8).cuda()
+        member = (torch.rand((B, P), generator=g) < 0.6).to(torch.uint8).cuda()
+        if it == 5:
+            member.zero_()  # bootstrap: no keyframe members -> keyframe
+        T = [0.3, 0.7, 0.9, 1.01][it % 4]
+        c1 = torch.zeros((B, 2), dtype=torch.int32, device="cuda")
+        c2 = torch.zeros_like(c1)
+        f1 = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        f2 = torch.zeros_like(f1)
+        t1 = torch.zeros((2,), dtype=torch.int64, device="cuda")
+        t2 = torch.zeros_like(t1)
+        v2d.survival_decide(status, member, c1, T, f1, done, t1, kf)
+        v2d.track_survival(status, member, c2)
+        v2d.keyframe_decide(c2, T, f2, t2)
+        torch.cuda.synchronize()
+        assert torch.equal(c1, c2) and torch.equal(f1, f2) and torch.equal(t1, t2), it
+        assert int(done.item()) == 0
+        n_kf += int(f2.item())
+    assert int(kf.item()) == n_kf
