@@ -745,7 +745,10 @@ __device__ __forceinline__ void track_level(float* __restrict__ sp, const Plane 
 }
 
 template <int WIN, bool kEachStep>
-__global__ void __launch_bounds__(kThreads, 16)
+#ifndef V2D_KLT_MINB
+#define V2D_KLT_MINB 15  // 136 registers: K3 -0.5 % at c5, -0.7 % at c2 vs 16 (128); 12 is +13 %
+#endif
+__global__ void __launch_bounds__(kThreads, V2D_KLT_MINB)
 klt_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __restrict__ prev_pyr,
            const uint8_t* const* __restrict__ next_l0, const float* const* __restrict__ next_pyr,
            int B, Levels lv, KltArgs a, const float* __restrict__ pts,
