@@ -556,7 +556,10 @@ __device__ __forceinline__ void ptrack_level(float* __restrict__ sp, const PPlan
 }
 
 template <int WIN, bool kEachStep>
-__global__ void __launch_bounds__(32, 16)
+#ifndef V2D_PAIR_MINB
+#define V2D_PAIR_MINB 16
+#endif
+__global__ void __launch_bounds__(32, V2D_PAIR_MINB)
 klt_pair_kernel(const uint8_t* const* __restrict__ prev_l0, const float* const* __restrict__ prev_pyr,
                 const uint8_t* const* __restrict__ next_l0, const float* const* __restrict__ next_pyr,
                 int B, Levels lv, KltArgs a, const float* __restrict__ pts,
